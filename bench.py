@@ -1,0 +1,330 @@
+#!/usr/bin/env python
+"""Benchmark: batched <H> + adjoint gradient circuits/s (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl tcx|reference] [--config I]
+
+One step = one tcx_grad_batch over the rank's theta batch (every row: forward window
+passes, lambda = H psi, adjoint backward passes, fp64 reductions) followed by the NCCL
+all-reduce of the loss sum_b E_b and the batch-summed gradient (north_star: "final NCCL
+all-reduce of loss and gradient").  Default workload: BASELINE configs[1] (n=20 Heisenberg
+VQE, HEA depth 10, B=1024 theta per rank, complex64).  Scaling: weak (B per rank fixed).
+For N > 1 launch with torchrun (one process per GPU, MASTER_ADDR=127.0.0.1).
+`--impl reference` times the CPU oracle (oracle/, the tier's reference arm) on host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def load_peaks():
+    try:
+        with open(PEAKS) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi samples during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+        self.th = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.th.join(timeout=2)
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = max(smax, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# -------------------------------------------------------------- reference
+def cpu_oracle_rows(circ, H, theta, threads):
+    from oracle import oracle as orc
+    t0 = time.perf_counter()
+    orc.value_grad_batch(circ, H, theta, nthreads=threads)
+    return time.perf_counter() - t0
+
+
+def run_reference(args, rank, world):
+    """The tier's reference arm: the CPU oracle, as it stands, on host cores."""
+    if rank != 0:
+        return 0
+    name, circ, H, theta, dtype = W.config(args.config, B=args.batch)
+    cores = os.cpu_count() or 1
+    rows = max(1, min(cores, args.ref_rows))
+    sample = theta[:rows]
+    for _ in range(args.warmup):
+        cpu_oracle_rows(circ, H, sample[:1], 1)
+    total = 0.0
+    for _ in range(args.steps):
+        total += cpu_oracle_rows(circ, H, sample, rows)
+    value = rows * args.steps / total
+    unit = "circuits/s"
+    line = {
+        "metric": "batched <H>+grad circuits/s (%s)" % name, "value": value, "unit": unit,
+        "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": name, "global_batch": rows, "seq_len": None,
+                   "parallelism": "oracle: OpenMP over theta rows"},
+        "cpu_baseline": {"value": value, "unit": unit, "cores": rows, "kind": "oracle",
+                         "sample": f"{rows} theta rows of {name} per step (one per core)"},
+        "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="tcx", choices=["tcx", "reference"])
+    ap.add_argument("--config", type=int, default=1, help="BASELINE.json configs index")
+    ap.add_argument("--batch", type=int, default=None, help="theta rows per rank")
+    ap.add_argument("--tile-bits", type=int, default=0)
+    ap.add_argument("--max-ops-per-pass", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-rows", type=int, default=8)
+    ap.add_argument("--cpu-rows", type=int, default=8)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "tcx" else args.warmup
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2205_10091_b200 import tcx
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+
+    name, circ, H, theta, dtype = W.config(args.config, B=args.batch)
+    B = theta.shape[0]
+    if world > 1 and rank > 0:  # distinct seeded rows per rank (weak scaling)
+        theta = W.thetas(B, circ.n_params, 1000 + rank) if args.config != 2 else \
+            W.qaoa_thetas(B, 5, 1000 + rank)
+    C = tcx.Circuit(circ, dtype, tile_bits=args.tile_bits, max_ops_per_pass=args.max_ops_per_pass)
+    P = tcx.Pauli(H)
+    info = C.info(P)
+    th = torch.as_tensor(np.ascontiguousarray(theta)).to(dev)
+    E = torch.empty(B, dtype=torch.float64, device=dev)
+    G = torch.empty(B, max(circ.n_params, 1), dtype=torch.float64, device=dev)
+    red = torch.empty(1 + circ.n_params, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    ws = tcx.Workspace()
+
+    def step():
+        tcx.grad_batch(C, P, th, stream=stream, ws=ws, out=(E, G))
+        red[0] = E.sum()
+        red[1:] = G[:, :circ.n_params].sum(0)
+        if world > 1:
+            dist.all_reduce(red)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    tcx.profile_enable(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    tcx.profile_enable(False)
+    prof = tcx.profile_read()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = world * B * args.steps / (ms / 1e3)
+
+    # ---- end to end through the host-buffer public API (pinned host memory)
+    th_h = torch.as_tensor(np.ascontiguousarray(theta)).pin_memory()
+    E_h = torch.empty(B, dtype=torch.float64).pin_memory()
+    G_h = torch.empty(B, max(circ.n_params, 1), dtype=torch.float64).pin_memory()
+    ws2 = tcx.Workspace()
+
+    def e2e_step():
+        tcx.grad_batch_host(C, P, th_h.numpy(), E_h.numpy(), G_h.numpy(), stream=stream, ws=ws2,
+                            device=dev)
+    e2e_step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_step()
+    e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e_value = world * B * args.steps / float(e2e_s.item())
+
+    # ---- roofline of the dominant kernel class
+    peaks, peak_src = load_peaks()
+    by = {}
+    for ph, idx, kms, fl, by_ in prof:
+        d = by.setdefault(ph, [0.0, 0.0, 0.0, 0])
+        d[0] += kms
+        d[1] += fl
+        d[2] += by_
+        d[3] += 1
+    total_k = sum(v[0] for v in by.values()) or 1.0
+    dom = max(by, key=lambda k: by[k][0]) if by else None
+    roof = None
+    if dom:
+        kms, fl, byt, cnt = by[dom]
+        lanes = 64 if dtype == "c128" else 128
+        alu_peak = 148 * lanes * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6  # flop/s
+        hbm_peak = peaks.get("hbm_gbs", 6650.0) * 1e9
+        t_alu, t_hbm = fl / alu_peak, byt / hbm_peak
+        if t_alu >= t_hbm:
+            ach = fl / (kms / 1e3) / 1e12
+            roof = {"bound": "alu", "achieved": ach, "peak": alu_peak / 1e12, "unit": "TFLOP/s",
+                    "frac": ach / (alu_peak / 1e12)}
+        else:
+            ach = byt / (kms / 1e3) / 1e9
+            roof = {"bound": "hbm", "achieved": ach, "peak": hbm_peak / 1e9, "unit": "GB/s",
+                    "frac": ach / (hbm_peak / 1e9)}
+        roof.update({"kernel": f"pass_kernel ({dom} passes)", "launches": cnt,
+                     "share_of_step": kms / total_k, "peak_source": peak_src,
+                     "hbm_achieved_gbs": byt / (kms / 1e3) / 1e9,
+                     "traffic": load_traffic(args.config, dom, cnt, args.steps)})
+    kernel_split = {k: {"ms": v[0] / args.steps, "launches_per_step": v[3] / args.steps,
+                        "tflops": v[1] / max(v[0], 1e-9) / 1e9, "gbs": v[2] / max(v[0], 1e-9) / 1e6}
+                    for k, v in by.items()}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = os.cpu_count() or 1
+        rows = max(1, min(cores, args.cpu_rows))
+        secs = cpu_oracle_rows(circ, H, theta[:rows], rows)
+        cpu = {"value": rows / secs, "unit": "circuits/s", "cores": rows, "kind": "oracle",
+               "sample": f"{rows} theta rows of {name} (one OpenMP thread per row), {secs:.1f} s"}
+
+    launches = C.launch_count(P, B, True) * args.steps
+    line = {
+        "metric": "batched <H>+grad circuits/s (%s)" % name,
+        "value": value, "unit": "circuits/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c64" if dtype == "c64" else "c128",
+        "data": "synthetic",
+        "config": {"workload": name, "global_batch": B * world, "batch_per_gpu": B,
+                   "seq_len": None, "parallelism": f"theta-batch dp{world}",
+                   "n_qubits": circ.n, "n_params": circ.n_params, "n_gates": len(circ.gates),
+                   "pauli_terms": int(len(H.weights)),
+                   "l2": "inputs larger than L2 (psi+lambda %.1f GiB per GPU)" % (
+                       2 * B * (2 ** circ.n) * (8 if dtype == "c64" else 16) / 2 ** 30),
+                   "plan": {k: info[k] for k in ("tile_bits", "reg_bits", "fwd_passes",
+                                                 "lambda_passes", "bwd_passes", "stages",
+                                                 "n_ops")}},
+        "roofline": roof,
+        "kernels": kernel_split,
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "circuits/s",
+                "h2d_bytes_per_step": int(B * circ.n_params * 8),
+                "d2h_bytes_per_step": int(B * 8 + B * circ.n_params * 8)},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def load_traffic(cfg, phase, launches, steps):
+    """DRAM traffic per launch of the dominant kernel from a committed ncu capture
+    (profiles/traffic.json, written from `ncu --set full`), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            d = json.load(f)
+        return d.get(f"cfg{cfg}", {}).get(phase)
+    except Exception:
+        return None
+
+
+if __name__ == "__main__":
+    sys.exit(main())

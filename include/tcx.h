@@ -1,0 +1,216 @@
+/*
+ * tcx.h -- C ABI of the B200-native batched <H> + grad engine (libtcx.so).
+ *
+ * The operation (arXiv 2205.10091, TensorCircuit):
+ *   psi_b = U_L(theta_b) ... U_1(theta_b) |0...0>          PAPER.md:391 (§3.3 default
+ *           input), :268-280 (§3.2 circuit + state()), north_star "contracting the
+ *           circuit's gate tensors into the 2^n-amplitude state tensor".
+ *   E_b   = Re sum_j alpha_j <psi_b|P_j|psi_b>              PAPER.md:79-91 (Eq. 1-2),
+ *           Pauli structures PAPER.md:794-815 (§6.2.1).
+ *   grad_b = dE_b/dtheta_b (per row)                        PAPER.md:487-492 (§4
+ *           value_and_grad), batched with argnums = vectorized_argnums = 0 as in the
+ *           batched-VQE example PAPER.md:1121-1139 (§6.3.5); obtained by an adjoint
+ *           reverse sweep (north_star step 4).
+ *
+ * Conventions (SURVEY.md §8 conventions):
+ *   - qubit 0 is the most significant bit of the amplitude index:
+ *     r = sum_q b_q 2^(n-1-q).
+ *   - rotations R_P(a) = exp(-i a P / 2), P in {X,Y,Z,XX,YY,ZZ}; a = coeff*theta[param]
+ *     when param >= 0, a = coeff when param == -1 (fixed angle).  PAPER.md:362's
+ *     exp1(theta, G) = e^{+i theta G} is R_GG with coeff = -2.
+ *   - two-qubit matrices on (q0, q1) use row/column index 2*b_q0 + b_q1
+ *     (PAPER.md:368-374); CNOT control = q0, target = q1.
+ *   - Pauli codes 0=I 1=X 2=Y 3=Z per qubit in paper order; weights real
+ *     ("alpha_j are real coefficients").
+ *   - complex amplitudes are interleaved (re, im): float2 for TCX_C64, double2 for
+ *     TCX_C128 (complex64 default / complex128).
+ *   - theta, E and grad are float64 for both dtypes.
+ *
+ * Ownership: the caller owns every buffer (theta, E, grad, state, workspace); the
+ * library owns the opaque handles.  Handles are immutable after build and may be
+ * shared across threads and streams.  All device work is enqueued on the caller's
+ * CUDA stream (cudaStream_t passed as void*; NULL = legacy default stream); no call
+ * synchronizes the device except the *_host variants, which synchronize the stream
+ * before returning.
+ *
+ * Errors: every entry returns a tcx_status; the library never aborts.  On failure
+ * tcx_last_error() (thread-local) names the offending argument / gate / term index.
+ * There is no CPU fallback: every compute step runs in the library's sm_100a kernels;
+ * without a usable CUDA device the compute entries return TCX_E_CUDA.
+ */
+#ifndef TCX_ABI_H_
+#define TCX_ABI_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    TCX_OK = 0,
+    TCX_E_INVALID = 1,      /* bad argument, gate, term, size, or workspace too small */
+    TCX_E_UNSUPPORTED = 2,  /* valid input outside this build's scope (e.g. grad of a
+                               non-unitary payload, C11 in DESIGN.md) */
+    TCX_E_OOM = 3,          /* host allocation failed */
+    TCX_E_CUDA = 4,         /* CUDA runtime error / no device */
+    TCX_E_NCCL = 5
+} tcx_status;
+
+typedef enum { TCX_C64 = 0, TCX_C128 = 1 } tcx_dtype;
+
+typedef enum {
+    /* fixed 1-qubit */
+    TCX_I = 0, TCX_X, TCX_Y, TCX_Z, TCX_H, TCX_S, TCX_SDG, TCX_T, TCX_TDG,
+    /* fixed 2-qubit */
+    TCX_CNOT, TCX_CZ, TCX_SWAP,
+    /* rotations R_P(coeff*theta[param]) */
+    TCX_RX, TCX_RY, TCX_RZ, TCX_RXX, TCX_RYY, TCX_RZZ,
+    /* fixed payload matrices (PAPER.md:355-360 c.unitary): 2x2 / 4x4 */
+    TCX_U1, TCX_U2,
+    TCX_NKINDS
+} tcx_gate_kind;
+
+/* One gate of the input list (32 bytes).
+ *   kind    tcx_gate_kind
+ *   q0, q1  qubits (q1 = -1 for 1-qubit gates); distinct, in [0, n)
+ *   param   theta column for rotations, -1 = fixed angle (then coeff is the angle);
+ *           must be -1 for non-rotation kinds
+ *   coeff   angle multiplier (rotations); ignored otherwise
+ *   payload offset in complex elements into `matrices` for TCX_U1 (4) / TCX_U2 (16),
+ *           -1 otherwise */
+typedef struct {
+    int32_t kind, q0, q1, param;
+    double coeff;
+    int64_t payload;
+} tcx_gate;
+
+/* Build options; zero-initialised = defaults chosen per dtype and n. */
+typedef struct {
+    int32_t tile_bits;      /* t: amplitudes per tile = 2^t (default 12 c64 / 11 c128; n if n<t) */
+    int32_t reg_bits;       /* r: amplitudes per thread per stage = 2^r (default 4, 3 if n<=t) */
+    int32_t coalesce_bits;  /* c: low index bits present in every tile (default: 64 B runs) */
+    int32_t max_ops_per_pass; /* fusion depth cap: 0 = light-cone (unlimited), 1 = unfused */
+    int32_t reserved[4];
+} tcx_build_opts;
+
+/* Executed-plan summary (for reports and tests). */
+typedef struct {
+    int32_t n_qubits, n_params, dtype;
+    int32_t tile_bits, reg_bits, coalesce_bits, threads_per_tile;
+    int32_t n_ops;            /* fused kernel ops after lowering */
+    int32_t fwd_passes;       /* F: forward window passes */
+    int32_t lambda_passes;    /* extra passes to complete lambda = H psi (excl. the last fwd) */
+    int32_t bwd_passes;       /* R */
+    int32_t stages;           /* register stages summed over forward passes */
+    int32_t unitary;          /* 1 if every payload is unitary (grad allowed) */
+    int32_t relabeled;        /* 1 if SWAP gates were applied as qubit relabels */
+    int64_t tiles_per_state;  /* 2^(n-t) */
+    int64_t acc_slots;        /* gradient partial slots per tile */
+    int64_t mat_reals;        /* per-theta materialised matrix entries */
+} tcx_plan_info;
+
+typedef struct tcx_circuit tcx_circuit;
+typedef struct tcx_pauli tcx_pauli;
+
+/* Compile a gate list into an executable plan (host only; the analog of K.jit,
+ * PAPER.md:492-496; excluded from timings as the paper excludes JIT).
+ * matrices: n_matrix_elems complex numbers as interleaved (re, im) float64, row-major,
+ * index order of the conventions above.  TCX_E_INVALID names the first bad gate. */
+tcx_status tcx_circuit_build(int32_t n_qubits, int32_t n_params,
+                             const tcx_gate* gates, int64_t n_gates,
+                             const double* matrices, int64_t n_matrix_elems,
+                             tcx_dtype dtype, const tcx_build_opts* opts,
+                             tcx_circuit** out);
+
+/* Pauli sum H = sum_j weights[j] P_j.  codes: [n_terms][n_qubits]
+ * uint8 in {0,1,2,3}, paper qubit order.  The identity string is allowed. */
+tcx_status tcx_pauli_build(int32_t n_qubits, int32_t n_terms, const uint8_t* codes,
+                           const double* weights, tcx_pauli** out);
+
+enum { TCX_WS_GRAD = 1, TCX_WS_HOST_IO = 2, TCX_WS_STATE = 4 };
+
+/* Device workspace bytes for a batch of B rows.  mode: TCX_WS_GRAD for tcx_grad_batch
+ * (psi and lambda), 0 for tcx_expect_batch, TCX_WS_STATE for tcx_state_batch; OR
+ * TCX_WS_HOST_IO for the *_host entries (adds device room for theta/E/grad). */
+tcx_status tcx_workspace_bytes(const tcx_circuit* circ, const tcx_pauli* pauli, int64_t B,
+                               int32_t mode, size_t* bytes);
+
+/* E[b] = Re sum_j alpha_j <psi(theta_b)|P_j|psi(theta_b)> for b < B.
+ * theta: device [B][n_params] float64 row-major; E: device [B] float64;
+ * ws: device workspace of >= tcx_workspace_bytes(..., 0) bytes. */
+tcx_status tcx_expect_batch(const tcx_circuit* circ, const tcx_pauli* pauli,
+                            const double* theta, int64_t B, double* E,
+                            void* ws, size_t ws_bytes, void* cuda_stream);
+
+/* E as above and grad[b][p] = dE_b/dtheta_{b,p} (per row).
+ * grad: device [B][n_params] float64.  TCX_E_UNSUPPORTED if a payload is not unitary
+ * (the adjoint sweep applies U^dagger). */
+tcx_status tcx_grad_batch(const tcx_circuit* circ, const tcx_pauli* pauli,
+                          const double* theta, int64_t B, double* E, double* grad,
+                          void* ws, size_t ws_bytes, void* cuda_stream);
+
+/* psi(theta_b) for b < B into state: device [B][2^n] complex (dtype of the circuit),
+ * paper index order (qubit 0 most significant), for parity tests. */
+tcx_status tcx_state_batch(const tcx_circuit* circ, const double* theta, int64_t B,
+                           void* state, void* ws, size_t ws_bytes, void* cuda_stream);
+
+/* End-to-end variants: theta/E/grad are HOST pointers (pinned memory recommended);
+ * the call copies theta host->device, runs the same kernels, copies E/grad back and
+ * synchronizes the stream.  ws must be sized with TCX_WS_HOST_IO. */
+tcx_status tcx_expect_batch_host(const tcx_circuit* circ, const tcx_pauli* pauli,
+                                 const double* theta_host, int64_t B, double* E_host,
+                                 void* ws, size_t ws_bytes, void* cuda_stream);
+tcx_status tcx_grad_batch_host(const tcx_circuit* circ, const tcx_pauli* pauli,
+                               const double* theta_host, int64_t B, double* E_host,
+                               double* grad_host, void* ws, size_t ws_bytes,
+                               void* cuda_stream);
+
+/* Plan summary. */
+tcx_status tcx_circuit_info(const tcx_circuit* circ, const tcx_pauli* pauli,
+                            tcx_plan_info* out);
+
+/* Decoded, validated gate table exactly as the plan stores it (bit-exact round trip
+ * of the input list; parse parity test).  Writes min(cap, n_gates) gates. */
+tcx_status tcx_circuit_decode(const tcx_circuit* circ, tcx_gate* out, int64_t cap,
+                              int64_t* n_gates);
+
+/* Physical index bit of each qubit at the end of the circuit (after SWAP relabels);
+ * out: [n_qubits].  Identity layout is bit = n-1-q. */
+tcx_status tcx_circuit_layout(const tcx_circuit* circ, int32_t* out);
+
+/* Kernel launches one tcx_grad_batch / tcx_expect_batch call enqueues for B rows. */
+tcx_status tcx_launch_count(const tcx_circuit* circ, const tcx_pauli* pauli, int64_t B,
+                            int32_t want_grad, int32_t* launches);
+
+/* Per-launch device timing (bench.py roofline).  When enabled on the calling thread,
+ * every kernel a compute entry enqueues is bracketed by CUDA events recorded on the
+ * call's stream.  tcx_profile_read waits for the recorded events, returns up to cap
+ * entries (oldest first) and clears the log.  flops / bytes are the launch's
+ * ALGORITHMIC floating-point operations and HBM bytes. */
+typedef struct {
+    int32_t phase;   /* 0 materialize, 1 forward pass, 2 lambda pass, 3 backward pass,
+                        4 finalize, 5 fused single pass (forward + lambda + backward) */
+    int32_t index;   /* pass / lambda-unit index */
+    float ms;
+    float pad;
+    double flops;
+    double bytes;
+} tcx_kernel_time;
+tcx_status tcx_profile_enable(int32_t on);
+tcx_status tcx_profile_read(tcx_kernel_time* out, int32_t cap, int32_t* n);
+
+void tcx_circuit_free(tcx_circuit* circ);
+void tcx_pauli_free(tcx_pauli* pauli);
+
+/* Thread-local message for the last failing call on this thread ("" if none). */
+const char* tcx_last_error(void);
+
+/* Library version string. */
+const char* tcx_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TCX_ABI_H_ */

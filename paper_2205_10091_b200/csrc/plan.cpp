@@ -1,0 +1,957 @@
+// plan.cpp -- circuit compiler: validation, lowering to fused ops on physical bits,
+// light-cone window scheduling, register-stage scheduling, table layout.
+//
+// Method references:
+//  * gate semantics: PAPER.md:343-386 (§3.2 gates, exp1, unitary), SURVEY §8 conventions.
+//  * "fuses runs of gates on low qubits into one pass" (north_star step 1): every pass
+//    runs all remaining ops whose non-diagonal bits lie in its window and that are not
+//    blocked by an earlier unrun op on a shared bit (SURVEY §8a "Window scheduling").
+//  * the reverse sweep replays the same passes/stages backwards (SURVEY §8a-7, R = F).
+#include "plan.h"
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <numeric>
+#include <set>
+
+namespace tcx {
+namespace {
+
+using cd = std::complex<double>;
+
+bool is_rot(int k) {
+  return k == TCX_RX || k == TCX_RY || k == TCX_RZ || k == TCX_RXX || k == TCX_RYY ||
+         k == TCX_RZZ;
+}
+bool is_2q(int k) {
+  return k == TCX_CNOT || k == TCX_CZ || k == TCX_SWAP || k == TCX_RXX || k == TCX_RYY ||
+         k == TCX_RZZ || k == TCX_U2;
+}
+bool is_diag1(int k) {
+  return k == TCX_I || k == TCX_Z || k == TCX_S || k == TCX_SDG || k == TCX_T ||
+         k == TCX_TDG || k == TCX_RZ;
+}
+inline int popc64(uint64_t x) { return __builtin_popcountll(x); }
+
+bool unitary_check(const double* m, int d) {
+  double worst = 0;
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < d; ++j) {
+      cd s = 0;
+      for (int k = 0; k < d; ++k)
+        s += std::conj(cd(m[2 * (k * d + i)], m[2 * (k * d + i) + 1])) *
+             cd(m[2 * (k * d + j)], m[2 * (k * d + j) + 1]);
+      if (i == j) s -= 1.0;
+      worst = std::max(worst, std::abs(s));
+    }
+  return worst < 1e-9;
+}
+
+// ------------------------------------------------------------------ lowering
+struct Lowerer {
+  Plan& P;
+  struct Run {
+    bool open = false, diag = true;
+    std::vector<Constituent> cons;
+  };
+  Run runs[kMaxQubits];
+  int last_on_bit[kMaxQubits];
+  int last_diag = -1;
+  explicit Lowerer(Plan& p) : P(p) { std::fill(last_on_bit, last_on_bit + kMaxQubits, -1); }
+
+  void emit(Op&& op) {
+    int idx = (int)P.ops.size();
+    for (int b = 0; b < P.n; ++b)
+      if (op.bits >> b & 1) last_on_bit[b] = idx;
+    if (op.type == OP_DIAG) last_diag = idx;
+    P.ops.push_back(std::move(op));
+  }
+  void emit_diag(const std::vector<DiagTerm>& terms, uint64_t bits) {
+    if (terms.empty()) return;
+    int lastS = -1;
+    for (int b = 0; b < P.n; ++b)
+      if (bits >> b & 1) lastS = std::max(lastS, last_on_bit[b]);
+    bool par = false;
+    for (auto& t : terms) par |= t.param >= 0;
+    if (last_diag >= 0 && last_diag >= lastS) {
+      Op& d = P.ops[last_diag];
+      d.terms.insert(d.terms.end(), terms.begin(), terms.end());
+      d.bits |= bits;
+      d.has_param |= par;
+      for (int b = 0; b < P.n; ++b)
+        if (bits >> b & 1) last_on_bit[b] = last_diag;
+      return;
+    }
+    Op op;
+    op.type = OP_DIAG;
+    op.bits = bits;
+    op.need = 0;
+    op.terms = terms;
+    op.has_param = par;
+    emit(std::move(op));
+  }
+  // exp(i w (-1)^{b}) factors of the diagonal 1-qubit gates (global phase kept so
+  // that state-level parity holds): Z = e^{i pi/2 (1 - Z)}, S = e^{i pi/4 (1 - Z)},
+  // T = e^{i pi/8 (1 - Z)}, RZ(a) = e^{-i a/2 Z}.
+  void diag_terms_of(const Constituent& c, int bit, std::vector<DiagTerm>& out) {
+    const uint64_t m = 1ull << bit;
+    auto fixed2 = [&](double w) {
+      out.push_back({0, -1, w});
+      out.push_back({m, -1, -w});
+    };
+    switch (c.kind) {
+      case TCX_I: break;
+      case TCX_Z: fixed2(M_PI / 2); break;
+      case TCX_S: fixed2(M_PI / 4); break;
+      case TCX_SDG: fixed2(-M_PI / 4); break;
+      case TCX_T: fixed2(M_PI / 8); break;
+      case TCX_TDG: fixed2(-M_PI / 8); break;
+      case TCX_RZ: out.push_back({m, c.param, -c.coeff / 2}); break;
+      default: break;
+    }
+  }
+  void add1(int bit, const Constituent& c, bool diag) {
+    Run& R = runs[bit];
+    R.open = true;
+    R.diag = R.diag && diag;
+    R.cons.push_back(c);
+  }
+  void close(int bit) {
+    Run& R = runs[bit];
+    if (!R.open) return;
+    if (R.diag) {
+      std::vector<DiagTerm> terms;
+      for (auto& c : R.cons) diag_terms_of(c, bit, terms);
+      emit_diag(terms, 1ull << bit);
+    } else {
+      Op op;
+      op.type = OP_U1;
+      op.bits = op.need = 1ull << bit;
+      op.b0 = bit;
+      op.cons = R.cons;
+      for (auto& c : op.cons) op.has_param |= c.param >= 0;
+      emit(std::move(op));
+    }
+    R = Run();
+  }
+};
+
+void normalize_diag(Op& op) {
+  // combine fixed terms by mask and param terms by (param, mask)
+  std::map<std::pair<int, uint64_t>, double> acc;
+  for (auto& t : op.terms) acc[{t.param, t.mask}] += t.w;
+  std::vector<DiagTerm> fixed, par;
+  for (auto& kv : acc) {
+    DiagTerm t{kv.first.second, kv.first.first, kv.second, -1};
+    if (t.param < 0) {
+      if (t.w != 0.0) fixed.push_back(t);
+    } else {
+      par.push_back(t);
+    }
+  }
+  // gradient slots: distinct (param, w)
+  std::map<std::pair<int, double>, int> slots;
+  for (auto& t : par) {
+    auto key = std::make_pair(t.param, t.w);
+    auto it = slots.find(key);
+    if (it == slots.end()) it = slots.emplace(key, (int)slots.size()).first;
+    t.slot = it->second;
+  }
+  std::stable_sort(par.begin(), par.end(),
+                   [](const DiagTerm& a, const DiagTerm& b) { return a.slot < b.slot; });
+  op.terms = fixed;
+  op.terms.insert(op.terms.end(), par.begin(), par.end());
+  op.nslots = (int)slots.size();
+  op.has_param = !par.empty();
+}
+
+// ------------------------------------------------------------- scheduling
+double op_weight(const Op& o) {
+  switch (o.type) {
+    case OP_U1: return 8.0;
+    case OP_U2F: return 16.0;
+    case OP_CX: return 1.0;
+    default: return 2.0 + 4.0 * (double)o.terms.size();
+  }
+}
+int op_mats(const Op& o) {
+  switch (o.type) {
+    case OP_U1: return 8;
+    case OP_U2F: return 32;
+    case OP_CX: return 0;
+    default: return 2 * (int)o.terms.size();
+  }
+}
+int op_accs(const Op& o) {
+  if (!o.has_param) return 0;
+  return o.type == OP_U1 ? 8 : o.nslots;
+}
+
+struct Budget {
+  int mats, accs, ops;
+};
+
+struct Scheduler {
+  Plan& P;
+  std::vector<char> done;
+  int first = 0;
+  uint64_t full;
+  Budget pass_budget;
+  explicit Scheduler(Plan& p) : P(p), done(p.ops.size(), 0) {
+    full = (P.n >= 64) ? ~0ull : ((1ull << P.n) - 1);
+  }
+  // light-cone closure under tile mask W (physical)
+  double closure(uint64_t W, std::vector<int>* out) {
+    uint64_t blocked = 0;
+    double score = 0;
+    int mats = 0, accs = 0, nops = 0;
+    for (int i = first; i < (int)P.ops.size(); ++i) {
+      if (done[i]) continue;
+      const Op& o = P.ops[i];
+      bool ok = !(o.bits & blocked) && !(o.need & ~W);
+      if (ok) {
+        int m2 = mats + op_mats(o), a2 = accs + op_accs(o);
+        if (m2 > pass_budget.mats || a2 > pass_budget.accs ||
+            (pass_budget.ops > 0 && nops + 1 > pass_budget.ops))
+          ok = false;
+        else {
+          mats = m2;
+          accs = a2;
+          nops++;
+          score += op_weight(o);
+          if (out) out->push_back(i);
+        }
+      }
+      if (!ok) {
+        blocked |= o.bits;
+        if ((blocked & full) == full) break;
+      }
+    }
+    return score;
+  }
+  // first not-runnable op's needed bits (guides window growth)
+  uint64_t first_missing(uint64_t W) {
+    uint64_t blocked = 0;
+    for (int i = first; i < (int)P.ops.size(); ++i) {
+      if (done[i]) continue;
+      const Op& o = P.ops[i];
+      if (!(o.bits & blocked) && (o.need & ~W)) return o.need & ~W;
+      if ((o.bits & blocked) || (o.need & ~W)) blocked |= o.bits;
+    }
+    return 0;
+  }
+  uint64_t choose_window() {
+    const int n = P.n, t = P.t, c = P.c;
+    if (n <= t) return full;
+    const uint64_t base = (1ull << c) - 1;
+    uint64_t bestW = 0;
+    double best = -1;
+    auto consider = [&](uint64_t W) {
+      double s = closure(W, nullptr);
+      if (s > best) {
+        best = s;
+        bestW = W;
+      }
+    };
+    auto fill = [&](uint64_t W) {  // pad with lowest unused bits
+      for (int b = 0; b < n && popc64(W) < t; ++b) W |= 1ull << b;
+      return W;
+    };
+    // (a) greedy growth by score
+    {
+      uint64_t W = base;
+      while (popc64(W) < t) {
+        double cur = closure(W, nullptr), bs = -1;
+        int bb = -1;
+        for (int b = 0; b < n; ++b) {
+          if (W >> b & 1) continue;
+          double s = closure(W | (1ull << b), nullptr);
+          if (s > bs) {
+            bs = s;
+            bb = b;
+          }
+        }
+        if (bs <= cur) {
+          uint64_t miss = first_missing(W);
+          uint64_t add = 0;
+          for (int b = 0; b < n; ++b)
+            if (miss >> b & 1) {
+              add = 1ull << b;
+              break;
+            }
+          if (!add) {
+            W = fill(W);
+            break;
+          }
+          W |= add;
+        } else {
+          W |= 1ull << bb;
+        }
+      }
+      consider(W);
+    }
+    // (b) earliest-need-first
+    {
+      uint64_t W = base;
+      for (int i = first; i < (int)P.ops.size() && popc64(W) < t; ++i) {
+        if (done[i]) continue;
+        uint64_t nw = W | P.ops[i].need;
+        if (popc64(nw) <= t) W = nw;
+      }
+      consider(fill(W));
+    }
+    // (c) contiguous runs above the coalescing bits
+    for (int s = c; s + (t - c) <= n; ++s) {
+      uint64_t W = base;
+      for (int b = s; b < s + (t - c); ++b) W |= 1ull << b;
+      consider(W);
+    }
+    return bestW;
+  }
+};
+
+// combinations helper
+void combos(int t, int r, std::vector<uint32_t>& out) {
+  for (uint32_t m = 0; m < (1u << t); ++m)
+    if (__builtin_popcount(m) == r) out.push_back(m);
+}
+
+struct StageOut {
+  uint32_t Rloc;                 // local register-bit mask
+  std::vector<int> ops;          // plan op indices
+};
+
+// Stage scheduling inside one pass: ops run in the stage whose register set covers
+// their non-diagonal bits (relaxed locality for CX controls and diagonals).
+void schedule_stages(Plan& P, const PassInfo& pass, std::vector<StageOut>& stages) {
+  const int t = P.t, r = P.r, h = P.h;
+  std::vector<int> loc(P.n, -1);
+  for (int l = 0; l < t; ++l) loc[pass.W[l]] = l;
+  auto lneed = [&](const Op& o) {  // register-slot need (U2F runs through smem)
+    uint32_t m = 0;
+    if (o.type == OP_U2F) return m;
+    for (int b = 0; b < P.n; ++b)
+      if (o.need >> b & 1) m |= 1u << loc[b];
+    return m;
+  };
+  std::vector<uint32_t> need(pass.ops.size());
+  for (size_t i = 0; i < pass.ops.size(); ++i) need[i] = lneed(P.ops[pass.ops[i]]);
+  std::vector<char> done(pass.ops.size(), 0);
+  size_t remaining = pass.ops.size();
+  const int kStageAccMax = 256;
+  auto closure = [&](uint32_t R, std::vector<int>* out) {
+    uint64_t blocked = 0;
+    double s = 0;
+    int accs = 0;
+    for (size_t i = 0; i < pass.ops.size(); ++i) {
+      if (done[i]) continue;
+      const Op& o = P.ops[pass.ops[i]];
+      bool ok = !(o.bits & blocked) && !(need[i] & ~R);
+      if (ok && accs + op_accs(o) > kStageAccMax) ok = false;
+      if (ok) {
+        accs += op_accs(o);
+        s += op_weight(o);
+        if (out) out->push_back((int)i);
+      } else {
+        blocked |= o.bits;
+      }
+    }
+    return s;
+  };
+  std::vector<uint32_t> cand;
+  combos(t, r, cand);
+  const uint32_t top = ((1u << t) - 1) & ~((1u << h) - 1);
+  bool first = true;
+  while (remaining > 0 || first) {
+    uint32_t R = top;
+    if (!first) {
+      double best = -1;
+      for (uint32_t m : cand) {
+        double s = closure(m, nullptr);
+        if (s > best) {
+          best = s;
+          R = m;
+        }
+      }
+    }
+    std::vector<int> idx;
+    closure(R, &idx);
+    StageOut so;
+    so.Rloc = R;
+    for (int i : idx) {
+      done[i] = 1;
+      so.ops.push_back(pass.ops[i]);
+    }
+    remaining -= idx.size();
+    if (!first && idx.empty()) break;  // cannot happen (r >= arity); guard
+    stages.push_back(std::move(so));
+    first = false;
+  }
+}
+
+// thread-bit order: lanes first, chosen so the lane bits' bank vectors are independent
+void thread_order(uint32_t Rloc, int t, bool c128, int8_t* T) {
+  const int lg = c128 ? 3 : 4;
+  std::vector<int> nr;
+  for (int l = 0; l < t; ++l)
+    if (!(Rloc >> l & 1)) nr.push_back(l);
+  std::vector<int> lanes, rest;
+  // greedy GF(2) basis over bank bits
+  std::vector<uint32_t> basis;
+  auto bankvec = [&](int l) { return swizzle_bit(l, c128) & ((1u << lg) - 1); };
+  auto indep = [&](uint32_t v) {
+    for (uint32_t b : basis) v = std::min(v, v ^ b);
+    return v != 0 ? v : 0u;
+  };
+  for (int l : nr) {
+    if ((int)lanes.size() < lg) {
+      uint32_t v = indep(bankvec(l));
+      if (v) {
+        // keep basis reduced
+        basis.push_back(v);
+        std::sort(basis.rbegin(), basis.rend());
+        lanes.push_back(l);
+        continue;
+      }
+    }
+    rest.push_back(l);
+  }
+  int m = 0;
+  for (int l : lanes) T[m++] = (int8_t)l;
+  for (int l : rest) T[m++] = (int8_t)l;
+}
+
+}  // namespace
+
+// Swizzle of the tile-local element index in shared memory: the low lg bits (bank
+// group within a 128-byte row) are XORed with a GF(2)-linear image of the higher bits,
+// chosen so that any (t - r) positions span the bank space.
+uint32_t swizzle_bit(int p, bool c128) {
+  static const uint32_t col64[] = {3, 5, 6, 9, 10, 12, 7, 11, 13, 14, 15, 3, 5};
+  static const uint32_t col128[] = {3, 5, 6, 7, 1, 2, 4, 3, 5, 6, 7, 1, 2};
+  const int lg = c128 ? 3 : 4;
+  if (p < lg) return 1u << p;
+  return (1u << p) ^ (c128 ? col128[p - lg] : col64[p - lg]);
+}
+
+tcx_status build_pauli(int n, int T, const uint8_t* codes, const double* w, Pauli& p,
+                       std::string& err) {
+  if (n < 1 || n > kMaxQubits) {
+    err = "pauli: n_qubits out of range";
+    return TCX_E_INVALID;
+  }
+  if (T < 0 || (T > 0 && (!codes || !w))) {
+    err = "pauli: bad term arrays";
+    return TCX_E_INVALID;
+  }
+  p.n = n;
+  p.codes.assign(codes, codes + (size_t)T * n);
+  p.weights.assign(w, w + T);
+  for (int j = 0; j < T; ++j) {
+    if (!std::isfinite(w[j])) {
+      err = "pauli: term " + std::to_string(j) + " has a non-finite weight";
+      return TCX_E_INVALID;
+    }
+    for (int q = 0; q < n; ++q)
+      if (codes[(size_t)j * n + q] > 3) {
+        err = "pauli: term " + std::to_string(j) + " qubit " + std::to_string(q) +
+              " has code > 3";
+        return TCX_E_INVALID;
+      }
+  }
+  return TCX_OK;
+}
+
+tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const double* mats,
+                      int64_t nmat, tcx_dtype dtype, const tcx_build_opts* opts, Plan& P,
+                      std::string& err) {
+  if (n < 1 || n > 34) {
+    err = "n_qubits must be in [1, 34]";
+    return TCX_E_INVALID;
+  }
+  if (Pn < 0 || G < 0 || (G > 0 && !gates) || nmat < 0 || (nmat > 0 && !mats)) {
+    err = "bad sizes or null arrays";
+    return TCX_E_INVALID;
+  }
+  if (dtype != TCX_C64 && dtype != TCX_C128) {
+    err = "dtype must be TCX_C64 or TCX_C128";
+    return TCX_E_INVALID;
+  }
+  P.n = n;
+  P.P = Pn;
+  P.dtype = dtype;
+  P.gates.assign(gates, gates + G);
+  P.mats_in.assign(mats, mats + 2 * nmat);
+  // ---- validate (SPEC.md:301 "arity mismatch; qubit out of range", :422 op index)
+  for (int64_t g = 0; g < G; ++g) {
+    const tcx_gate& x = gates[g];
+    auto bad = [&](const char* why) {
+      err = "gate " + std::to_string(g) + ": " + why;
+      return TCX_E_INVALID;
+    };
+    if (x.kind < 0 || x.kind >= TCX_NKINDS) return bad("unknown kind");
+    if (x.q0 < 0 || x.q0 >= n) return bad("q0 out of range");
+    if (is_2q(x.kind)) {
+      if (x.q1 < 0 || x.q1 >= n) return bad("q1 out of range");
+      if (x.q1 == x.q0) return bad("q0 == q1");
+    } else if (x.q1 != -1) {
+      return bad("q1 must be -1 for a 1-qubit gate");
+    }
+    if (is_rot(x.kind)) {
+      if (x.param < -1 || x.param >= Pn) return bad("param out of range");
+      if (!std::isfinite(x.coeff)) return bad("non-finite coeff");
+    } else if (x.param != -1) {
+      return bad("param must be -1 for a non-rotation gate");
+    }
+    if (x.kind == TCX_U1 || x.kind == TCX_U2) {
+      int64_t need = x.kind == TCX_U1 ? 4 : 16;
+      if (x.payload < 0 || x.payload + need > nmat) return bad("payload out of range");
+      for (int64_t e = 0; e < 2 * need; ++e)
+        if (!std::isfinite(mats[2 * x.payload + e])) return bad("non-finite payload");
+    } else if (x.payload != -1) {
+      return bad("payload must be -1 for this kind");
+    }
+  }
+  // ---- options
+  const bool c128 = dtype == TCX_C128;
+  int tdef = c128 ? 11 : 12;
+  int t = opts && opts->tile_bits > 0 ? opts->tile_bits : tdef;
+  int c = opts && opts->coalesce_bits > 0 ? opts->coalesce_bits : (c128 ? 2 : 3);
+  t = std::min(t, kMaxTileBits);
+  if (t >= n) t = n;
+  int r = opts && opts->reg_bits > 0 ? opts->reg_bits : (t < tdef ? 3 : 4);
+  r = std::min(r, kMaxRegBits);
+  if (r > t) r = t;
+  if (t - r > 8) r = t - 8;  // at most 256 threads per tile (kernel launch bounds)
+  if (r > kMaxRegBits) {
+    err = "tile_bits too large: needs reg_bits <= 4 with <= 256 threads (t <= 12)";
+    return TCX_E_INVALID;
+  }
+  if (c > t) c = t;
+  if (n > t && t - c < 2) {
+    err = "tile_bits - coalesce_bits must be >= 2";
+    return TCX_E_INVALID;
+  }
+  P.t = t;
+  P.r = r;
+  P.c = c;
+  P.h = t - r;
+  P.max_ops_per_pass = opts ? std::max(0, opts->max_ops_per_pass) : 0;
+  P.tiles = 1ll << (n - t);
+  // ---- lower
+  int pos[kMaxQubits];
+  for (int q = 0; q < n; ++q) pos[q] = n - 1 - q;  // PAPER.md:249 qubit 0 = MSB
+  Lowerer L(P);
+  auto payload_copy = [&](int64_t off, int d) {
+    int64_t at = (int64_t)P.fixed.size() / 2;
+    for (int64_t e = 0; e < 2 * d * d; ++e) P.fixed.push_back(mats[2 * off + e]);
+    if (!unitary_check(mats + 2 * off, d)) P.unitary = false;
+    return at;
+  };
+  for (int64_t g = 0; g < G; ++g) {
+    const tcx_gate& x = gates[g];
+    if (!is_2q(x.kind)) {
+      if (x.kind == TCX_I) continue;
+      Constituent cn{x.kind, is_rot(x.kind) ? x.param : -1, x.coeff, -1, -1};
+      if (x.kind == TCX_U1) cn.payload = payload_copy(x.payload, 2);
+      L.add1(pos[x.q0], cn, is_diag1(x.kind));
+      continue;
+    }
+    const int a = pos[x.q0], b = pos[x.q1];
+    const uint64_t ab = (1ull << a) | (1ull << b);
+    switch (x.kind) {
+      case TCX_SWAP:
+        std::swap(pos[x.q0], pos[x.q1]);
+        P.relabeled = true;
+        break;
+      case TCX_CNOT: {
+        L.close(a);
+        L.close(b);
+        Op op;
+        op.type = OP_CX;
+        op.bits = ab;
+        op.need = 1ull << b;
+        op.b0 = b;  // target
+        op.b1 = a;  // control
+        L.emit(std::move(op));
+        break;
+      }
+      case TCX_CZ:
+        L.close(a);
+        L.close(b);
+        // CZ = exp(i pi/4 (1 - Z_a - Z_b + Z_a Z_b))
+        L.emit_diag({{0, -1, M_PI / 4},
+                     {1ull << a, -1, -M_PI / 4},
+                     {1ull << b, -1, -M_PI / 4},
+                     {ab, -1, M_PI / 4}},
+                    ab);
+        break;
+      case TCX_RZZ:
+        L.close(a);
+        L.close(b);
+        L.emit_diag({{ab, x.param, -x.coeff / 2}}, ab);
+        break;
+      case TCX_RXX:
+      case TCX_RYY: {
+        // R_XX(a) = (H x H) R_ZZ(a) (H x H);  R_YY(a) = (V^+ x V^+) R_ZZ(a) (V x V),
+        // V = R_X(pi/2) (V^+ Z V = Y).
+        Constituent pre{TCX_H, -1, 0.0, -1, -1}, post{TCX_H, -1, 0.0, -1, -1};
+        if (x.kind == TCX_RYY) {
+          pre = {TCX_RX, -1, M_PI / 2, -1, -1};
+          post = {TCX_RX, -1, -M_PI / 2, -1, -1};
+        }
+        L.add1(a, pre, false);
+        L.add1(b, pre, false);
+        L.close(a);
+        L.close(b);
+        L.emit_diag({{ab, x.param, -x.coeff / 2}}, ab);
+        L.add1(a, post, false);
+        L.add1(b, post, false);
+        break;
+      }
+      case TCX_U2: {
+        L.close(a);
+        L.close(b);
+        Op op;
+        op.type = OP_U2F;
+        op.bits = op.need = ab;
+        op.b0 = a;  // index 2*b_q0 + b_q1
+        op.b1 = b;
+        op.u2_payload = payload_copy(x.payload, 4);
+        L.emit(std::move(op));
+        break;
+      }
+    }
+  }
+  for (int b = 0; b < n; ++b) L.close(b);
+  for (auto& op : P.ops)
+    if (op.type == OP_DIAG) normalize_diag(op);
+  for (int q = 0; q < n; ++q) P.layout[q] = pos[q];
+
+  // ---- pass scheduling
+  Scheduler S(P);
+  const int rb = c128 ? 8 : 4;  // bytes per Real
+  S.pass_budget.mats = (24 * 1024) / rb;
+  S.pass_budget.accs = 2048;
+  S.pass_budget.ops = P.max_ops_per_pass;
+  size_t left = P.ops.size();
+  while (left > 0) {
+    uint64_t W = S.choose_window();
+    std::vector<int> list;
+    S.closure(W, &list);
+    if (list.empty()) {
+      err = "internal scheduler error (no progress)";
+      return TCX_E_INVALID;
+    }
+    PassInfo pi;
+    pi.wmask = W;
+    int l = 0;
+    for (int b = 0; b < n; ++b)
+      if (W >> b & 1) pi.W[l++] = b;
+    pi.ops = list;
+    for (int i : list) {
+      S.done[i] = 1;
+      P.ops[i].pass = (int)P.passes.size();
+    }
+    while (S.first < (int)P.ops.size() && S.done[S.first]) S.first++;
+    left -= list.size();
+    P.passes.push_back(std::move(pi));
+  }
+  if (P.passes.empty()) {  // empty circuit: one init pass
+    PassInfo pi;
+    pi.wmask = (t >= 64) ? ~0ull : ((1ull << t) - 1);
+    for (int l = 0; l < t; ++l) pi.W[l] = l;
+    P.passes.push_back(pi);
+  }
+
+  // ---- stages, kernel tables, matrix and accumulator layout
+  int mat = 0, acc = 0;
+  for (auto& pass : P.passes) {
+    std::vector<StageOut> stages;
+    schedule_stages(P, pass, stages);
+    pass.stage_begin = (int)P.kstages.size();
+    pass.kop_begin = (int)P.kops.size();
+    pass.kterm_begin = (int)P.kterms.size();
+    pass.mat_begin = mat;
+    pass.acc_begin = acc;
+    std::vector<int> loc(n, -1);
+    for (int l = 0; l < t; ++l) loc[pass.W[l]] = l;
+    int pass_acc = 0;
+    uint32_t prevR = 0xFFFFFFFFu;
+    for (auto& st : stages) {
+      KStage ks;
+      std::memset(&ks, 0, sizeof(ks));
+      int k = 0;
+      for (int l = 0; l < t; ++l)
+        if (st.Rloc >> l & 1) ks.R[k++] = (int8_t)l;
+      if (st.Rloc == (((1u << t) - 1) & ~((1u << P.h) - 1)) && &st == &stages[0]) {
+        for (int m = 0; m < P.h; ++m) ks.T[m] = (int8_t)m;  // load/store mapping
+      } else {
+        thread_order(st.Rloc, t, c128, ks.T);
+      }
+      ks.same_as_prev = 0;
+      if (!P.kstages.empty() && (int)P.kstages.size() > pass.stage_begin) {
+        const KStage& pv = P.kstages.back();
+        ks.same_as_prev = (std::memcmp(pv.R, ks.R, sizeof(ks.R)) == 0 &&
+                           std::memcmp(pv.T, ks.T, sizeof(ks.T)) == 0) ? 1 : 0;
+      }
+      (void)prevR;
+      ks.op_begin = (int)P.kops.size() - pass.kop_begin;
+      ks.acc_begin = pass_acc;
+      int stage_acc = 0;
+      auto slot_of = [&](int bit) {
+        int l = loc[bit];
+        for (int j = 0; j < P.r; ++j)
+          if (ks.R[j] == l) return j;
+        return -1;
+      };
+      for (int oi : st.ops) {
+        Op& o = P.ops[oi];
+        KOp ko;
+        std::memset(&ko, 0, sizeof(ko));
+        ko.type = o.type;
+        ko.acc = -1;
+        ko.term = -1;
+        o.mat_off = mat;
+        o.mat_len = op_mats(o);
+        ko.mat = (int16_t)(mat - pass.mat_begin);
+        if (o.type == OP_U1) {
+          ko.a = (uint8_t)slot_of(o.b0);
+        } else if (o.type == OP_U2F) {  // tile-local positions (shared-memory op)
+          ko.a = (uint8_t)loc[o.b0];
+          ko.b = (uint8_t)loc[o.b1];
+        } else if (o.type == OP_CX) {
+          ko.a = (uint8_t)slot_of(o.b0);
+          int cs = loc[o.b1] >= 0 ? slot_of(o.b1) : -1;
+          ko.b = cs >= 0 ? (uint8_t)cs : kExtCtrl;
+          ko.cbit = (uint8_t)o.b1;
+        } else {
+          ko.nterm = (int16_t)o.terms.size();
+          ko.term = (int)P.kterms.size() - pass.kterm_begin;
+          for (size_t i = 0; i < o.terms.size(); ++i) {
+            KTerm kt;
+            std::memset(&kt, 0, sizeof(kt));
+            kt.mask = o.terms[i].mask;
+            kt.wofs = (int16_t)(mat - pass.mat_begin + 2 * (int)i);
+            kt.acc = o.terms[i].param >= 0 ? (int16_t)(stage_acc + o.terms[i].slot) : -1;
+            P.kterms.push_back(kt);
+          }
+        }
+        int na = op_accs(o);
+        if (na > 0) {
+          ko.acc = stage_acc;
+          o.acc_off = pass.acc_begin + pass_acc + stage_acc;
+          o.acc_len = na;
+          stage_acc += na;
+        }
+        mat += o.mat_len;
+        P.kops.push_back(ko);
+      }
+      ks.op_count = (int)P.kops.size() - pass.kop_begin - ks.op_begin;
+      ks.acc_count = stage_acc;
+      pass_acc += stage_acc;
+      pass.max_stage_acc = std::max(pass.max_stage_acc, stage_acc);
+      P.kstages.push_back(ks);
+    }
+    pass.stage_count = (int)P.kstages.size() - pass.stage_begin;
+    {
+      const KStage& ls = P.kstages.back();
+      bool top = true;
+      for (int k = 0; k < P.r; ++k) top &= ls.R[k] == P.h + k;
+      for (int m = 0; m < P.h; ++m) top &= ls.T[m] == m;
+      pass.last_is_top = top ? 1 : 0;
+    }
+    pass.kop_count = (int)P.kops.size() - pass.kop_begin;
+    pass.kterm_count = (int)P.kterms.size() - pass.kterm_begin;
+    pass.mat_count = mat - pass.mat_begin;
+    pass.acc_count = pass_acc;
+    acc += pass_acc;
+  }
+  P.mat_total = mat;
+  P.acc_total = acc;
+
+  // ---- materialize / finalize tables
+  int contrib = 0;
+  std::vector<int> contrib_param;
+  for (auto& o : P.ops) {
+    if (o.type == OP_U1) {
+      MItem mi{};
+      mi.type = OP_U1;
+      mi.mat_off = o.mat_off;
+      mi.cons_begin = (int)P.dcons.size();
+      mi.cons_count = (int)o.cons.size();
+      mi.param = -1;
+      for (auto& cn : o.cons) {
+        DCons d{};
+        d.kind = cn.kind;
+        d.param = cn.param;
+        d.coeff = cn.coeff;
+        d.payload = cn.payload;
+        d.contrib = -1;
+        if (cn.param >= 0) {
+          d.contrib = contrib++;
+          contrib_param.push_back(cn.param);
+        }
+        P.dcons.push_back(d);
+      }
+      P.mitems.push_back(mi);
+      if (o.has_param) {
+        GItem gi{};
+        gi.type = OP_U1;
+        gi.acc = o.acc_off;
+        gi.cons_begin = mi.cons_begin;
+        gi.cons_count = mi.cons_count;
+        gi.contrib = -1;
+        P.gitems.push_back(gi);
+      }
+    } else if (o.type == OP_U2F) {
+      MItem mi{};
+      mi.type = OP_U2F;
+      mi.mat_off = o.mat_off;
+      mi.payload = o.u2_payload;
+      mi.param = -1;
+      P.mitems.push_back(mi);
+    } else if (o.type == OP_DIAG) {
+      for (size_t i = 0; i < o.terms.size(); ++i) {
+        MItem mi{};
+        mi.type = OP_DIAG;
+        mi.mat_off = o.mat_off + 2 * (int)i;
+        mi.param = o.terms[i].param;
+        mi.w = o.terms[i].w;
+        mi.payload = -1;
+        P.mitems.push_back(mi);
+      }
+      // one finalize item per gradient slot
+      std::vector<int> seen(o.nslots, 0);
+      for (auto& tm : o.terms) {
+        if (tm.param < 0 || seen[tm.slot]) continue;
+        seen[tm.slot] = 1;
+        GItem gi{};
+        gi.type = OP_DIAG;
+        gi.acc = o.acc_off + tm.slot;
+        gi.factor = -2.0 * tm.w;
+        gi.contrib = contrib++;
+        contrib_param.push_back(tm.param);
+        P.gitems.push_back(gi);
+      }
+    }
+  }
+  P.n_contrib = contrib;
+  P.param_ptr.assign(Pn + 1, 0);
+  for (int p : contrib_param) P.param_ptr[p + 1]++;
+  for (int p = 0; p < Pn; ++p) P.param_ptr[p + 1] += P.param_ptr[p];
+  P.param_list.assign(contrib, 0);
+  {
+    std::vector<int> fill(P.param_ptr.begin(), P.param_ptr.end() - 1);
+    for (int ci = 0; ci < contrib; ++ci) P.param_list[fill[contrib_param[ci]]++] = ci;
+  }
+  return TCX_OK;
+}
+
+// ---------------------------------------------------------------- binding
+std::shared_ptr<Binding> bind(Plan& P, const Pauli& H) {
+  auto B = std::make_shared<Binding>();
+  const int n = P.n, t = P.t, c = P.c;
+  // group terms by X/Y flip mask (physical bits through the final layout)
+  std::map<uint64_t, std::vector<KPTerm>> groups;
+  const int T = (int)H.weights.size();
+  for (int j = 0; j < T; ++j) {
+    uint64_t x = 0, zy = 0;
+    int ny = 0;
+    for (int q = 0; q < n; ++q) {
+      int code = H.codes[(size_t)j * n + q];
+      uint64_t bit = 1ull << P.layout[q];
+      if (code == 1 || code == 2) x |= bit;
+      if (code == 2 || code == 3) zy |= bit;
+      if (code == 2) ny++;
+    }
+    // (P psi)_r = i^nY (-1)^popc((r ^ x) & zy) psi_{r ^ x}   (SURVEY §8 conventions)
+    double re = 0, im = 0;
+    switch (ny & 3) {
+      case 0: re = 1; break;
+      case 1: im = 1; break;
+      case 2: re = -1; break;
+      case 3: im = -1; break;
+    }
+    double s = (popc64(x & zy) & 1) ? -1.0 : 1.0;
+    groups[x].push_back({zy, H.weights[j] * re * s, H.weights[j] * im * s});
+  }
+  // units: the last forward pass, then greedy windows for the remaining groups
+  std::vector<std::pair<uint64_t, std::vector<KPTerm>>> left(groups.begin(), groups.end());
+  const uint64_t full = (n >= 64) ? ~0ull : ((1ull << n) - 1);
+  bool gather_all = false;
+  auto add_unit = [&](uint64_t W, int fwd_pass) {
+    LamUnit u;
+    u.wmask = W;
+    int l = 0;
+    int loc[64];
+    for (int b = 0; b < n; ++b)
+      if (W >> b & 1) {
+        loc[b] = l;
+        u.W[l++] = b;
+      }
+    u.fwd_pass = fwd_pass;
+    u.group_begin = (int)B->groups.size();
+    std::vector<std::pair<uint64_t, std::vector<KPTerm>>> rest;
+    for (auto& g : left) {
+      const bool global = fwd_pass < 0 && gather_all;
+      if (global || (g.first & ~W) == 0) {
+        KGroup kg{};
+        uint32_t xl = 0;
+        if (!global)
+          for (int b = 0; b < n; ++b)
+            if (g.first >> b & 1) xl |= 1u << loc[b];
+        kg.xlocal = xl;
+        kg.xphys = g.first;
+        kg.global = global ? 1 : 0;
+        kg.term_begin = (int)B->pterms.size();
+        kg.term_count = (int)g.second.size();
+        B->pterms.insert(B->pterms.end(), g.second.begin(), g.second.end());
+        B->groups.push_back(kg);
+      } else {
+        rest.push_back(g);
+      }
+    }
+    u.group_count = (int)B->groups.size() - u.group_begin;
+    left.swap(rest);
+    B->units.push_back(u);
+  };
+  const PassInfo& last = P.passes.back();
+  add_unit(n <= t ? full : last.wmask, (int)P.passes.size() - 1);
+  while (!left.empty()) {
+    uint64_t W = (1ull << c) - 1;
+    // admit groups in order of fewest extra bits
+    bool grew = true;
+    while (grew) {
+      grew = false;
+      int best = -1, bestc = 1 << 30;
+      for (size_t i = 0; i < left.size(); ++i) {
+        uint64_t nw = W | left[i].first;
+        int cnt = popc64(nw);
+        if ((left[i].first & ~W) == 0 || cnt > t) continue;
+        if (cnt < bestc) {
+          bestc = cnt;
+          best = (int)i;
+        }
+      }
+      if (best >= 0) {
+        W |= left[best].first;
+        grew = true;
+      }
+    }
+    for (int b = 0; b < n && popc64(W) < t; ++b) W |= 1ull << b;
+    size_t before = left.size();
+    add_unit(W, -1);
+    if (left.size() == before) {
+      // flip masks wider than a window: one more unit gathers partners from HBM
+      gather_all = true;
+      B->units.pop_back();
+      add_unit(W, -1);
+    }
+  }
+  return B;
+}
+
+}  // namespace tcx

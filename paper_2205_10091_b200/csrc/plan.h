@@ -1,0 +1,193 @@
+// plan.h -- host-side circuit compiler for the tcx engine (the K.jit analog,
+// PAPER.md:492-496).  Lowers a gate list to fused kernel ops on physical index bits,
+// schedules light-cone window passes and register stages, and lays out the tables
+// the sm_100a kernels execute.  Pure host code: no CUDA calls here.
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/tcx.h"
+
+namespace tcx {
+
+enum : uint8_t { OP_U1 = 1, OP_U2F = 2, OP_CX = 3, OP_DIAG = 4 };
+constexpr int kMaxQubits = 40;
+constexpr int kMaxTileBits = 15;
+constexpr int kMaxRegBits = 4;
+constexpr uint8_t kExtCtrl = 0xFF;
+
+// One original 1-qubit gate folded into a fused U1 op (applied in list order).
+struct Constituent {
+  int32_t kind;     // tcx_gate_kind of a 1-qubit gate
+  int32_t param;    // theta column or -1
+  double coeff;     // rotation: angle multiplier (param>=0) or fixed angle
+  int64_t payload;  // complex offset into Plan::fixed for TCX_U1, else -1
+  int32_t contrib;  // gradient contribution index (param >= 0), else -1
+};
+
+// Diagonal op term: phase(r) *= exp(i * w_eff * (-1)^popc(r & mask)), where
+// w_eff = w (param < 0) or w * theta[param].  R_Z-type gates exp(-i a Z_m / 2) with
+// a = coeff*theta give w = -coeff/2.
+struct DiagTerm {
+  uint64_t mask;
+  int32_t param;
+  double w;
+  int32_t slot = -1;  // op-local gradient slot (param terms sharing (param, w))
+};
+
+struct Op {
+  uint8_t type = 0;
+  uint64_t bits = 0;  // every physical bit the op reads (dependencies)
+  uint64_t need = 0;  // bits that must be inside the tile / register set
+  int b0 = -1, b1 = -1;  // U1: bit; U2F: (hi=q0, lo=q1); CX: (target, control)
+  std::vector<Constituent> cons;  // U1
+  int64_t u2_payload = -1;        // U2F
+  std::vector<DiagTerm> terms;    // DIAG
+  int nslots = 0;                 // DIAG: distinct gradient slots
+  bool has_param = false;
+  // layout (filled by the scheduler)
+  int pass = -1;
+  int mat_off = 0, mat_len = 0;  // Reals in the per-theta table
+  int acc_off = -1, acc_len = 0; // global partial slots
+};
+
+// ---- kernel tables (POD, copied to the device as-is) ----
+struct KOp {       // 16 bytes
+  uint8_t type, a, b, cbit;  // slots / external control bit
+  int16_t mat;     // offset (Reals) into the pass's smem matrix table
+  int16_t nterm;   // DIAG terms
+  int32_t acc;     // stage-local acc slot base, -1 none
+  int32_t term;    // DIAG: first KTerm (pass-relative)
+};
+struct KTerm {     // 16 bytes
+  uint64_t mask;   // physical bits
+  int16_t wofs;    // (cos, sin) pair offset in the pass matrix table
+  int16_t acc;     // stage-local acc slot, -1 none
+  int32_t pad;
+};
+struct KStage {    // 48 bytes
+  int8_t R[8];     // local positions of register slots k < r
+  int8_t T[16];    // local positions of thread bits m < h (lanes first)
+  int32_t op_begin, op_count;      // pass-relative KOp range
+  int32_t acc_begin, acc_count;    // pass-relative slot range
+  int32_t same_as_prev, pad;       // 1: identical mapping to the previous stage
+};
+struct KGroup {    // Pauli terms sharing one X/Y flip mask
+  uint64_t xphys;     // flip mask, physical bits
+  uint32_t xlocal;    // flip mask in tile-local bits (global == 0)
+  int32_t term_begin, term_count;
+  int32_t global;     // 1: partner amplitudes gathered from global memory
+};
+struct KPTerm {    // 24 bytes: coefficient alpha_j * i^nY * (-1)^popc(x & zy)
+  uint64_t zy;     // physical Y|Z mask
+  double cre, cim;
+};
+// materialize items (per theta): U1 product, U2F copy, diag (cos, sin)
+struct MItem {
+  int32_t type;      // OP_U1 / OP_U2F / OP_DIAG(term)
+  int32_t mat_off;   // Reals
+  int32_t cons_begin, cons_count;
+  int64_t payload;
+  int32_t param, pad;
+  double w;
+};
+struct DCons {       // device copy of Constituent
+  int32_t kind, param;
+  double coeff;
+  int64_t payload;
+  int32_t contrib, pad;
+};
+struct GItem {       // finalize items
+  int32_t type;      // OP_U1: R' -> constituent contributions; OP_DIAG: scalar slot
+  int32_t acc;       // global slot (U1: 8 slots)
+  int32_t cons_begin, cons_count;
+  double factor;     // DIAG: -2 * w
+  int32_t contrib, pad;
+};
+
+struct PassInfo {
+  uint64_t wmask = 0;
+  int W[kMaxTileBits + 1] = {0};   // local -> physical bit
+  std::vector<int> ops;             // plan op indices in program order
+  int stage_begin = 0, stage_count = 0;  // into Plan::kstages
+  int kop_begin = 0, kop_count = 0;      // into Plan::kops
+  int kterm_begin = 0, kterm_count = 0;  // into Plan::kterms
+  int mat_begin = 0, mat_count = 0;
+  int acc_begin = 0, acc_count = 0;
+  int max_stage_acc = 0;
+  int last_is_top = 1;   // last stage uses the load/store mapping
+};
+
+struct Pauli {
+  int n = 0;
+  std::vector<uint8_t> codes;  // [T][n]
+  std::vector<double> weights;
+};
+
+// Lambda evaluation unit: a window pass computing some Pauli groups.
+struct LamUnit {
+  uint64_t wmask = 0;
+  int W[kMaxTileBits + 1] = {0};
+  int group_begin = 0, group_count = 0;  // into Binding::groups
+  int fwd_pass = -1;   // >= 0: fused into this forward pass (the last one)
+};
+
+struct Binding {        // (circuit, pauli) specific lambda schedule
+  std::vector<KGroup> groups;
+  std::vector<KPTerm> pterms;
+  std::vector<LamUnit> units;
+  bool xmask_ok = true;
+  std::string err;
+  // device copies (per device)
+  std::map<int, std::pair<void*, void*>> dev;  // device -> (groups, pterms)
+};
+
+struct DeviceTables;
+
+struct Plan {
+  int n = 0, P = 0;
+  tcx_dtype dtype = TCX_C64;
+  int t = 0, r = 0, c = 0, h = 0;
+  int max_ops_per_pass = 0;
+  std::vector<tcx_gate> gates;  // validated input (decode)
+  std::vector<double> mats_in;  // input payloads
+  std::vector<double> fixed;    // complex (re, im) payloads referenced by ops
+  std::vector<Op> ops;
+  std::vector<PassInfo> passes;
+  std::vector<KOp> kops;
+  std::vector<KTerm> kterms;
+  std::vector<KStage> kstages;
+  std::vector<MItem> mitems;
+  std::vector<DCons> dcons;
+  std::vector<GItem> gitems;
+  std::vector<int32_t> param_ptr, param_list;  // CSR param -> contrib indices
+  int n_contrib = 0;
+  int mat_total = 0;
+  int acc_total = 0;
+  int layout[kMaxQubits] = {0};  // final physical bit of each qubit
+  bool relabeled = false;
+  bool unitary = true;
+  int64_t tiles = 1;             // 2^(n - t)
+
+  std::mutex mu;
+  std::map<const void*, std::shared_ptr<Binding>> bindings;
+  std::map<int, std::shared_ptr<DeviceTables>> dev;
+};
+
+// Build; returns TCX_OK or an error with message.
+tcx_status build_plan(int n, int P, const tcx_gate* gates, int64_t G, const double* mats,
+                      int64_t nmat, tcx_dtype dtype, const tcx_build_opts* opts, Plan& plan,
+                      std::string& err);
+tcx_status build_pauli(int n, int T, const uint8_t* codes, const double* w, Pauli& p,
+                       std::string& err);
+std::shared_ptr<Binding> bind(Plan& plan, const Pauli& pauli);
+
+// swizzled shared-memory bit table: sw(1 << p) for local position p
+uint32_t swizzle_bit(int p, bool c128);
+
+}  // namespace tcx

@@ -1,0 +1,905 @@
+// tcx.cu -- sm_100a kernels and the C ABI of libtcx.so.
+//
+// Hot path:
+//   materialize_kernel  per-theta fused gate matrices / diagonal phases (a2)
+//   pass_kernel<Real,RB> window pass over 2^t-amplitude tiles: forward gate stages
+//                       (a4), lambda = H psi + E partials fused into the last pass (a6),
+//                       adjoint backward stages with <lambda|dG|psi> partials (a7)
+//   finalize_kernel     deterministic fp64 reductions -> E[B], grad[B][P] (a8)
+// Every step of the path runs in these kernels; there is no host fallback.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <type_traits>
+
+#include "kernels.cuh"
+#include "plan.h"
+
+using namespace tcx;
+
+namespace {
+
+thread_local std::string g_err;
+tcx_status fail(tcx_status s, const std::string& m) {
+  g_err = m;
+  return s;
+}
+struct ProfEntry {
+  int phase, index;
+  cudaEvent_t a, b;
+  double flops, bytes;
+};
+struct ProfLog {
+  bool on = false;
+  std::vector<ProfEntry> log;
+};
+thread_local ProfLog g_prof;
+
+#define CUDA_TRY(x)                                                                    \
+  do {                                                                                 \
+    cudaError_t e_ = (x);                                                              \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(TCX_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));       \
+  } while (0)
+
+// ================================================================== device
+using namespace tcx::dev;
+
+// ---- per-theta gate matrices (fp64 math, stored in the state precision)
+struct cdd {
+  double x, y;
+};
+__device__ __forceinline__ cdd cmul(cdd a, cdd b) { return {a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x}; }
+__device__ __forceinline__ cdd cadd(cdd a, cdd b) { return {a.x + b.x, a.y + b.y}; }
+__device__ __forceinline__ cdd cconj(cdd a) { return {a.x, -a.y}; }
+
+// 1-qubit gate matrix g[0..3] (row-major) -- same conventions as tcx.h
+__device__ void gate1(const DCons& c, const double* theta, const double* fixed, cdd* g) {
+  const double r2 = 0.70710678118654752440;
+  const double a = c.param >= 0 ? c.coeff * theta[c.param] : c.coeff;
+  double cs, sn;
+  sincos(0.5 * a, &sn, &cs);
+  g[0] = {1, 0}; g[1] = {0, 0}; g[2] = {0, 0}; g[3] = {1, 0};
+  switch (c.kind) {
+    case TCX_X: g[0] = {0, 0}; g[1] = {1, 0}; g[2] = {1, 0}; g[3] = {0, 0}; break;
+    case TCX_Y: g[0] = {0, 0}; g[1] = {0, -1}; g[2] = {0, 1}; g[3] = {0, 0}; break;
+    case TCX_Z: g[3] = {-1, 0}; break;
+    case TCX_H: g[0] = {r2, 0}; g[1] = {r2, 0}; g[2] = {r2, 0}; g[3] = {-r2, 0}; break;
+    case TCX_S: g[3] = {0, 1}; break;
+    case TCX_SDG: g[3] = {0, -1}; break;
+    case TCX_T: g[3] = {r2, r2}; break;
+    case TCX_TDG: g[3] = {r2, -r2}; break;
+    case TCX_RX: g[0] = {cs, 0}; g[1] = {0, -sn}; g[2] = {0, -sn}; g[3] = {cs, 0}; break;
+    case TCX_RY: g[0] = {cs, 0}; g[1] = {-sn, 0}; g[2] = {sn, 0}; g[3] = {cs, 0}; break;
+    case TCX_RZ: g[0] = {cs, -sn}; g[1] = {0, 0}; g[2] = {0, 0}; g[3] = {cs, sn}; break;
+    case TCX_U1:
+      for (int i = 0; i < 4; ++i) g[i] = {fixed[2 * (c.payload + i)], fixed[2 * (c.payload + i) + 1]};
+      break;
+    default: break;
+  }
+}
+__device__ void mat2mul(const cdd* A, const cdd* B, cdd* O) {  // O = A B
+  cdd t[4];
+  for (int i = 0; i < 2; ++i)
+    for (int j = 0; j < 2; ++j) t[i * 2 + j] = cadd(cmul(A[i * 2], B[j]), cmul(A[i * 2 + 1], B[2 + j]));
+  for (int i = 0; i < 4; ++i) O[i] = t[i];
+}
+
+struct MatArgs {
+  const MItem* items;
+  int nitems;
+  const DCons* cons;
+  const double* fixed;
+  const double* theta;
+  int P;
+  void* mats;
+  int mat_total;
+};
+
+template <typename Real>
+__global__ void materialize_kernel(const MatArgs a) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.nitems) return;
+  const int64_t b = blockIdx.y;
+  const double* th = a.theta + b * a.P;
+  Real* out = reinterpret_cast<Real*>(a.mats) + b * a.mat_total;
+  const MItem it = a.items[i];
+  if (it.type == OP_U1) {
+    cdd M[4] = {{1, 0}, {0, 0}, {0, 0}, {1, 0}}, G[4];
+    for (int c = 0; c < it.cons_count; ++c) {
+      gate1(a.cons[it.cons_begin + c], th, a.fixed, G);
+      mat2mul(G, M, M);
+    }
+    for (int k = 0; k < 4; ++k) {
+      out[it.mat_off + 2 * k] = (Real)M[k].x;
+      out[it.mat_off + 2 * k + 1] = (Real)M[k].y;
+    }
+  } else if (it.type == OP_U2F) {
+    for (int k = 0; k < 32; ++k) out[it.mat_off + k] = (Real)a.fixed[2 * it.payload + k];
+  } else {
+    const double w = it.param >= 0 ? it.w * th[it.param] : it.w;
+    double s, c;
+    sincos(w, &s, &c);
+    out[it.mat_off] = (Real)c;
+    out[it.mat_off + 1] = (Real)s;
+  }
+}
+
+struct FinArgs {
+  const double* part;   // [B][S][K]
+  const double* epart;  // [B][S][EU]
+  int S, K, EU;
+  const GItem* gitems;
+  int ngitems;
+  const DCons* cons;
+  const double* fixed;
+  const double* theta;
+  int P;
+  const int32_t* pptr;
+  const int32_t* plist;
+  int ncontrib;
+  double* tot;          // [B][K]
+  double* contrib;      // [B][ncontrib]
+  double* E;
+  double* grad;         // may be null
+  int64_t b0;
+};
+
+// Deterministic fixed-order fp64 reductions (C10) and the gradient
+// contraction grad_g = coeff_g Im Tr(B_g R') with B_g = S_g P_g S_g^dagger,
+// S_g = G_m ... G_{g+1} (SURVEY §8a-5 block adjoint, restricted to 1-qubit blocks).
+__global__ void finalize_kernel(const FinArgs a) {
+  const int64_t b = a.b0 + blockIdx.x;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  __shared__ double red[256];
+  // E
+  {
+    double s = 0.0;
+    const int tot = a.S * a.EU;
+    const int per = (tot + nt - 1) / nt;
+    const double* src = a.epart + b * (int64_t)tot;
+    for (int i = tid * per; i < min(tot, (tid + 1) * per); ++i) s += src[i];
+    red[tid] = s;
+    __syncthreads();
+    if (tid == 0) {
+      double e = 0.0;
+      for (int i = 0; i < nt; ++i) e += red[i];
+      a.E[b] = e;
+    }
+  }
+  if (!a.grad) return;
+  const double* th = a.theta + b * a.P;
+  double* tot = a.tot + b * a.K;
+  for (int k = tid; k < a.K; k += nt) {
+    double s = 0.0;
+    const double* src = a.part + b * (int64_t)a.S * a.K + k;
+    for (int sl = 0; sl < a.S; ++sl) s += src[(int64_t)sl * a.K];
+    tot[k] = s;
+  }
+  __syncthreads();
+  double* ctb = a.contrib + b * a.ncontrib;
+  for (int gi = tid; gi < a.ngitems; gi += nt) {
+    const GItem g = a.gitems[gi];
+    if (g.type == OP_DIAG) {
+      ctb[g.contrib] = g.factor * tot[g.acc];
+      continue;
+    }
+    const cdd R[4] = {{tot[g.acc + 0], tot[g.acc + 1]}, {tot[g.acc + 2], tot[g.acc + 3]},
+                      {tot[g.acc + 4], tot[g.acc + 5]}, {tot[g.acc + 6], tot[g.acc + 7]}};
+    cdd Sfx[4] = {{1, 0}, {0, 0}, {0, 0}, {1, 0}};
+    for (int c = g.cons_count - 1; c >= 0; --c) {
+      const DCons cn = a.cons[g.cons_begin + c];
+      if (cn.param >= 0) {
+        cdd Pm[4] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+        if (cn.kind == TCX_RX) { Pm[1] = {1, 0}; Pm[2] = {1, 0}; }
+        if (cn.kind == TCX_RY) { Pm[1] = {0, -1}; Pm[2] = {0, 1}; }
+        if (cn.kind == TCX_RZ) { Pm[0] = {1, 0}; Pm[3] = {-1, 0}; }
+        cdd T1[4], Bm[4], Sd[4] = {cconj(Sfx[0]), cconj(Sfx[2]), cconj(Sfx[1]), cconj(Sfx[3])};
+        mat2mul(Sfx, Pm, T1);
+        mat2mul(T1, Sd, Bm);
+        // Tr(B R') = sum_ij B_ji R'_ij
+        cdd tr = {0, 0};
+        for (int i = 0; i < 2; ++i)
+          for (int j = 0; j < 2; ++j) tr = cadd(tr, cmul(Bm[j * 2 + i], R[i * 2 + j]));
+        ctb[cn.contrib] = cn.coeff * tr.y;
+      }
+      cdd G[4];
+      gate1(cn, th, a.fixed, G);
+      mat2mul(Sfx, G, Sfx);
+    }
+  }
+  __syncthreads();
+  for (int p = tid; p < a.P; p += nt) {
+    double s = 0.0;
+    for (int i = a.pptr[p]; i < a.pptr[p + 1]; ++i) s += ctb[a.plist[i]];
+    a.grad[b * a.P + p] = s;
+  }
+}
+
+// gather physical -> paper index order (only when SWAP relabels moved qubits)
+template <typename Real>
+__global__ void export_kernel(const Cx<Real>* src, Cx<Real>* dst, int n, int64_t total,
+                              const int* layout) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const int64_t N = 1ll << n;
+  const int64_t b = i >> n, r = i & (N - 1);
+  int64_t phys = 0;
+  for (int q = 0; q < n; ++q)
+    if ((r >> (n - 1 - q)) & 1) phys |= 1ll << layout[q];
+  dst[b * N + r] = src[b * N + phys];
+}
+
+// ================================================================== host
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+}  // namespace
+
+namespace tcx {
+struct DeviceTables {
+  DevBuf kops, kterms, kstages, mitems, dcons, gitems, pptr, plist, fixed, layout, swb;
+};
+}  // namespace tcx
+
+struct tcx_circuit {
+  Plan plan;
+};
+struct tcx_pauli {
+  Pauli p;
+};
+
+namespace {
+
+template <typename T>
+tcx_status upload(DevBuf& d, const std::vector<T>& v) {
+  size_t bytes = std::max<size_t>(sizeof(T) * v.size(), 16);
+  CUDA_TRY(cudaMalloc(&d.p, bytes));
+  if (!v.empty()) CUDA_TRY(cudaMemcpy(d.p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+  return TCX_OK;
+}
+
+tcx_status device_tables(Plan& P, DeviceTables*& out) {
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(P.mu);
+  auto it = P.dev.find(dev);
+  if (it != P.dev.end()) {
+    out = it->second.get();
+    return TCX_OK;
+  }
+  auto T = std::make_shared<DeviceTables>();
+  tcx_status s;
+  std::vector<uint32_t> swb(16);
+  for (int p = 0; p < 16; ++p) swb[p] = swizzle_bit(p, P.dtype == TCX_C128);
+  if ((s = upload(T->swb, swb))) return s;
+  if ((s = upload(T->kops, P.kops)) || (s = upload(T->kterms, P.kterms)) ||
+      (s = upload(T->kstages, P.kstages)) || (s = upload(T->mitems, P.mitems)) ||
+      (s = upload(T->dcons, P.dcons)) || (s = upload(T->gitems, P.gitems)) ||
+      (s = upload(T->pptr, P.param_ptr)) || (s = upload(T->plist, P.param_list)) ||
+      (s = upload(T->fixed, P.fixed)))
+    return s;
+  std::vector<int> lay(P.layout, P.layout + P.n);
+  if ((s = upload(T->layout, lay))) return s;
+  out = T.get();
+  P.dev[dev] = T;
+  return TCX_OK;
+}
+
+struct BindDev {
+  KGroup* groups;
+  KPTerm* pterms;
+};
+
+tcx_status binding_for(Plan& P, const tcx_pauli* H, std::shared_ptr<Binding>& out, BindDev* dv) {
+  {
+    std::lock_guard<std::mutex> lk(P.mu);
+    auto it = P.bindings.find(H);
+    if (it != P.bindings.end()) out = it->second;
+  }
+  if (!out) {
+    auto b = bind(P, H->p);
+    std::lock_guard<std::mutex> lk(P.mu);
+    auto it = P.bindings.find(H);
+    if (it != P.bindings.end())
+      out = it->second;
+    else
+      P.bindings[H] = out = b;
+  }
+  if (!out->xmask_ok) return fail(TCX_E_UNSUPPORTED, out->err);
+  if (dv) {
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(P.mu);
+    auto it = out->dev.find(dev);
+    if (it == out->dev.end()) {
+      void *g = nullptr, *t = nullptr;
+      size_t gb = std::max<size_t>(16, sizeof(KGroup) * out->groups.size());
+      size_t tb = std::max<size_t>(16, sizeof(KPTerm) * out->pterms.size());
+      CUDA_TRY(cudaMalloc(&g, gb));
+      CUDA_TRY(cudaMalloc(&t, tb));
+      if (!out->groups.empty())
+        CUDA_TRY(cudaMemcpy(g, out->groups.data(), sizeof(KGroup) * out->groups.size(), cudaMemcpyHostToDevice));
+      if (!out->pterms.empty())
+        CUDA_TRY(cudaMemcpy(t, out->pterms.data(), sizeof(KPTerm) * out->pterms.size(), cudaMemcpyHostToDevice));
+      it = out->dev.emplace(dev, std::make_pair(g, t)).first;
+    }
+    dv->groups = (KGroup*)it->second.first;
+    dv->pterms = (KPTerm*)it->second.second;
+  }
+  return TCX_OK;
+}
+
+int tiles_per_cta(const Plan& P) {
+  int64_t T = P.tiles;
+  int64_t tpc = std::min<int64_t>(64, std::max<int64_t>(1, T / 32));
+  return (int)tpc;
+}
+
+enum { K_EXPECT = 0, K_GRAD = 1, K_STATE = 2 };
+
+struct WsLayout {
+  size_t psi, lam, mats, part, epart, tot, contrib, theta, E, grad, total;
+  bool mega;
+};
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+WsLayout ws_layout(const Plan& P, const Binding* Bd, int64_t B, int kind, bool host_io) {
+  WsLayout w{};
+  const size_t rs = P.dtype == TCX_C128 ? 8 : 4;
+  const size_t N = size_t(1) << P.n;
+  const int64_t S = P.tiles / tiles_per_cta(P);
+  const int EU = Bd ? (int)Bd->units.size() : 1;
+  w.mega = kind != K_STATE && P.passes.size() == 1 && EU == 1;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align256(off + std::max<size_t>(bytes, 16));
+    return o;
+  };
+  const bool need_psi = !w.mega;
+  const bool need_lam = kind == K_GRAD && !w.mega;
+  w.psi = need_psi ? take(B * N * 2 * rs) : 0;
+  w.lam = need_lam ? take(B * N * 2 * rs) : 0;
+  w.mats = take(B * std::max(P.mat_total, 1) * rs);
+  w.part = kind == K_GRAD ? take(B * S * std::max(P.acc_total, 1) * 8) : 0;
+  w.epart = kind != K_STATE ? take(B * S * EU * 8) : 0;
+  w.tot = kind == K_GRAD ? take(B * std::max(P.acc_total, 1) * 8) : 0;
+  w.contrib = kind == K_GRAD ? take(B * std::max(P.n_contrib, 1) * 8) : 0;
+  if (host_io) {
+    w.theta = take(B * std::max(P.P, 1) * 8);
+    w.E = take(B * 8);
+    w.grad = kind == K_GRAD ? take(B * std::max(P.P, 1) * 8) : 0;
+  }
+  w.total = off;
+  return w;
+}
+
+// ---- algorithmic cost model: real flops per amplitude, complex
+// multiply = 6, complex add = 2.
+double op_flops(const Op& o, bool bwd) {
+  const double nt = (double)o.terms.size();
+  double npar = 0;
+  for (auto& t : o.terms) npar += t.param >= 0;
+  switch (o.type) {
+    case OP_U1: return bwd ? 28.0 + (o.has_param ? 16.0 : 0.0) : 14.0;
+    case OP_U2F: return bwd ? 60.0 : 30.0;
+    case OP_CX: return 0.0;
+    default: return bwd ? 12.0 * nt + 2.0 * npar : 6.0 * nt;
+  }
+}
+double pass_flops(const Plan& P, const PassInfo& p, bool bwd) {
+  double f = 0;
+  for (int i : p.ops) f += op_flops(P.ops[i], bwd);
+  return f;
+}
+double lambda_flops(const Binding& B, const LamUnit& u) {
+  double f = 4.0;
+  for (int g = u.group_begin; g < u.group_begin + u.group_count; ++g)
+    f += 8.0 + 2.0 * B.groups[g].term_count;
+  return f;
+}
+
+tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, double* E,
+               double* grad, void* state, void* ws, size_t ws_bytes, cudaStream_t st, int kind,
+               const WsLayout* wl_in) {
+  if (B <= 0) return fail(TCX_E_INVALID, "B must be > 0");
+  if (!ws) return fail(TCX_E_INVALID, "null workspace");
+  if (P.P > 0 && !theta) return fail(TCX_E_INVALID, "null theta");
+  if (kind != K_STATE && !E) return fail(TCX_E_INVALID, "null E");
+  if (kind == K_GRAD && P.P > 0 && !grad) return fail(TCX_E_INVALID, "null grad");
+  if (kind == K_STATE && !state) return fail(TCX_E_INVALID, "null state");
+  if (kind == K_GRAD && !P.unitary)
+    return fail(TCX_E_UNSUPPORTED, "grad needs unitary payloads (adjoint applies U^dagger)");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(TCX_E_CUDA, "no CUDA device (tcx has no CPU fallback)");
+  DeviceTables* DT = nullptr;
+  tcx_status s = device_tables(P, DT);
+  if (s) return s;
+  std::shared_ptr<Binding> Bd;
+  BindDev bdv{nullptr, nullptr};
+  if (kind != K_STATE) {
+    if (!H) return fail(TCX_E_INVALID, "null pauli");
+    if (H->p.n != P.n) return fail(TCX_E_INVALID, "pauli n_qubits != circuit n_qubits");
+    if ((s = binding_for(P, H, Bd, &bdv))) return s;
+  }
+  WsLayout wl = wl_in ? *wl_in : ws_layout(P, Bd.get(), B, kind, false);
+  if (ws_bytes < wl.total)
+    return fail(TCX_E_INVALID, "workspace too small: need " + std::to_string(wl.total) +
+                                   " bytes, got " + std::to_string(ws_bytes));
+  char* W = (char*)ws;
+  const bool c128 = P.dtype == TCX_C128;
+  const int rs = c128 ? 8 : 4;
+  const int64_t S = P.tiles / tiles_per_cta(P);
+  const int EU = Bd ? (int)Bd->units.size() : 1;
+  const int64_t kMaxRows = 65535;
+  // ---- materialize per-theta matrices
+  for (int64_t b0 = 0; b0 < B; b0 += kMaxRows) {
+    const int64_t rows = std::min(kMaxRows, B - b0);
+    if (P.mitems.empty()) break;
+    MatArgs ma;
+    ma.items = (const MItem*)DT->mitems.p;
+    ma.nitems = (int)P.mitems.size();
+    ma.cons = (const DCons*)DT->dcons.p;
+    ma.fixed = (const double*)DT->fixed.p;
+    ma.theta = theta + b0 * P.P;
+    ma.P = P.P;
+    ma.mats = W + wl.mats + b0 * P.mat_total * rs;
+    ma.mat_total = P.mat_total;
+    dim3 g((ma.nitems + 127) / 128, (unsigned)rows);
+    if (c128)
+      materialize_kernel<double><<<g, 128, 0, st>>>(ma);
+    else
+      materialize_kernel<float><<<g, 128, 0, st>>>(ma);
+    CUDA_TRY(cudaGetLastError());
+  }
+  // ---- pass launches
+  auto base_args = [&](PassArgs& a, uint64_t wmask, const int* Wl, int mode) {
+    std::memset(&a, 0, sizeof(a));
+    a.psi = W + wl.psi;
+    a.lam = W + wl.lam;
+    a.mats = W + wl.mats;
+    a.part = (double*)(W + wl.part);
+    a.epart = (double*)(W + wl.epart);
+    a.stages = (const KStage*)DT->kstages.p;
+    a.ops = (const KOp*)DT->kops.p;
+    a.terms = (const KTerm*)DT->kterms.p;
+    a.groups = bdv.groups;
+    a.pterms = bdv.pterms;
+    a.swb = (const uint32_t*)DT->swb.p;
+    a.wmask = wmask;
+    for (int l = 0; l < P.t; ++l) a.W[l] = Wl[l];
+    a.n = P.n;
+    a.t = P.t;
+    a.h = P.h;
+    a.mat_total = P.mat_total;
+    a.acc_total = std::max(P.acc_total, 1);
+    a.e_units = EU;
+    a.mode = mode;
+    a.tiles_per_cta = tiles_per_cta(P);
+    a.last_is_top = 1;
+  };
+  auto set_pass = [&](PassArgs& a, const PassInfo& p, bool with_ops) {
+    a.stages = (const KStage*)DT->kstages.p + p.stage_begin;
+    a.ops = (const KOp*)DT->kops.p + p.kop_begin;
+    a.terms = (const KTerm*)DT->kterms.p + p.kterm_begin;
+    a.nstages = with_ops ? p.stage_count : 0;
+    a.mat_begin = p.mat_begin;
+    a.mat_count = with_ops ? p.mat_count : 0;
+    a.acc_begin = p.acc_begin;
+    a.acc_count = p.acc_count;
+    a.max_stage_acc = p.max_stage_acc;
+    a.last_is_top = p.last_is_top;
+  };
+  auto launch_raw = [&](PassArgs& a) -> tcx_status {
+    const bool fwd = (a.mode & (M_FWD | M_LAMBDA)) != 0;
+    const bool two = (a.mode & M_BWD) != 0;
+    const int km = (fwd && two) ? KM_MEGA : (two ? KM_BWD : KM_FWD);
+    SmemLayout L = smem_layout(a.t, a.h, rs, a.mat_count, a.max_stage_acc,
+                               (a.mode & M_BWD) ? a.acc_count : 0, a.nstages, two);
+    if (!(a.mode & M_BWD)) {
+      a.acc_count = 0;
+      a.max_stage_acc = 0;
+      L = smem_layout(a.t, a.h, rs, a.mat_count, 0, 0, a.nstages, two);
+    }
+    if (L.total > 227 * 1024 - 256)
+      return fail(TCX_E_UNSUPPORTED, "pass needs " + std::to_string(L.total) +
+                                         " B of shared memory (> 227 KB); lower tile_bits");
+    for (int64_t b0 = 0; b0 < B; b0 += kMaxRows) {
+      const int64_t rows = std::min(kMaxRows, B - b0);
+      a.b0 = b0;
+      cudaError_t e;
+      if (c128)
+        e = km == 0 ? launch_f64_0(P.r, a, S, rows, L.total, st)
+                    : (km == 1 ? launch_f64_1(P.r, a, S, rows, L.total, st)
+                               : launch_f64_2(P.r, a, S, rows, L.total, st));
+      else
+        e = km == 0 ? launch_f32_0(P.r, a, S, rows, L.total, st)
+                    : (km == 1 ? launch_f32_1(P.r, a, S, rows, L.total, st)
+                               : launch_f32_2(P.r, a, S, rows, L.total, st));
+      if (e != cudaSuccess) return fail(TCX_E_CUDA, std::string("pass launch: ") + cudaGetErrorString(e));
+    }
+    return TCX_OK;
+  };
+  const double Nf = (double)((int64_t)1 << P.n), csz = 2.0 * rs, Bf = (double)B;
+  auto launch = [&](PassArgs& a, int phase, int index, double flops_amp) -> tcx_status {
+    ProfEntry pe{};
+    if (g_prof.on) {
+      CUDA_TRY(cudaEventCreate(&pe.a));
+      CUDA_TRY(cudaEventCreate(&pe.b));
+      CUDA_TRY(cudaEventRecord(pe.a, st));
+    }
+    tcx_status r0 = launch_raw(a);
+    if (r0) return r0;
+    if (g_prof.on) {
+      CUDA_TRY(cudaEventRecord(pe.b, st));
+      const int m = a.mode;
+      const double touches = ((m & M_LOAD_PSI) ? 1 : 0) + ((m & M_STORE_PSI) ? 1 : 0) +
+                             ((m & M_LOAD_LAM) ? 1 : 0) + ((m & M_STORE_LAM) ? 1 : 0);
+      pe.phase = phase;
+      pe.index = index;
+      pe.flops = Bf * Nf * flops_amp;
+      pe.bytes = Bf * Nf * csz * touches;
+      g_prof.log.push_back(pe);
+    }
+    return TCX_OK;
+  };
+  const int nP = (int)P.passes.size();
+  if (wl.mega) {
+    const PassInfo& p = P.passes[0];
+    PassArgs a;
+    int mode = M_INIT | M_FWD | M_LAMBDA | (kind == K_GRAD ? M_BWD : 0);
+    base_args(a, p.wmask, p.W, mode);
+    set_pass(a, p, true);
+    a.group_count = Bd->units[0].group_count;
+    a.groups = bdv.groups + Bd->units[0].group_begin;
+    a.e_index = 0;
+    const double fl = pass_flops(P, p, false) + lambda_flops(*Bd, Bd->units[0]) +
+                      (kind == K_GRAD ? pass_flops(P, p, true) : 0.0);
+    if ((s = launch(a, 5, 0, fl))) return s;
+  } else {
+    for (int pi = 0; pi < nP; ++pi) {
+      const PassInfo& p = P.passes[pi];
+      const bool last = pi == nP - 1;
+      int mode = M_FWD | M_STORE_PSI | (pi == 0 ? M_INIT : M_LOAD_PSI);
+      PassArgs a;
+      base_args(a, p.wmask, p.W, mode);
+      set_pass(a, p, true);
+      if (last && kind != K_STATE) {
+        a.mode |= M_LAMBDA | (kind == K_GRAD ? M_STORE_LAM : 0);
+        if (kind != K_GRAD && EU == 1) a.mode &= ~M_STORE_PSI;
+        a.group_count = Bd->units[0].group_count;
+        a.groups = bdv.groups + Bd->units[0].group_begin;
+        a.e_index = 0;
+      }
+      double fl = pass_flops(P, p, false);
+      if (last && kind != K_STATE) fl += lambda_flops(*Bd, Bd->units[0]);
+      if ((s = launch(a, 1, pi, fl))) return s;
+    }
+    if (kind != K_STATE) {
+      for (int u = 1; u < EU; ++u) {
+        const LamUnit& U = Bd->units[u];
+        PassArgs a;
+        int mode = M_LOAD_PSI | M_LAMBDA | (kind == K_GRAD ? (M_LOAD_LAM | M_STORE_LAM) : 0);
+        base_args(a, U.wmask, U.W, mode);
+        a.nstages = 0;
+        a.mat_count = 0;
+        a.acc_count = 0;
+        a.group_count = U.group_count;
+        a.groups = bdv.groups + U.group_begin;
+        a.e_index = u;
+        if ((s = launch(a, 2, u, lambda_flops(*Bd, U)))) return s;
+      }
+    }
+    if (kind == K_GRAD) {
+      for (int pi = nP - 1; pi >= 0; --pi) {
+        const PassInfo& p = P.passes[pi];
+        int mode = M_LOAD_PSI | M_LOAD_LAM | M_BWD | (pi > 0 ? (M_STORE_PSI | M_STORE_LAM) : 0);
+        PassArgs a;
+        base_args(a, p.wmask, p.W, mode);
+        set_pass(a, p, true);
+        if ((s = launch(a, 3, pi, pass_flops(P, p, true)))) return s;
+      }
+    }
+  }
+  // ---- finalize / export
+  if (kind != K_STATE) {
+    for (int64_t b0 = 0; b0 < B; b0 += kMaxRows) {
+      const int64_t rows = std::min(kMaxRows, B - b0);
+      FinArgs f;
+      f.part = (const double*)(W + wl.part);
+      f.epart = (const double*)(W + wl.epart);
+      f.S = (int)S;
+      f.K = std::max(P.acc_total, 1);
+      f.EU = EU;
+      f.gitems = (const GItem*)DT->gitems.p;
+      f.ngitems = (int)P.gitems.size();
+      f.cons = (const DCons*)DT->dcons.p;
+      f.fixed = (const double*)DT->fixed.p;
+      f.theta = theta;
+      f.P = P.P;
+      f.pptr = (const int32_t*)DT->pptr.p;
+      f.plist = (const int32_t*)DT->plist.p;
+      f.ncontrib = std::max(P.n_contrib, 1);
+      f.tot = (double*)(W + wl.tot);
+      f.contrib = (double*)(W + wl.contrib);
+      f.E = E;
+      f.grad = kind == K_GRAD && P.P > 0 ? grad : nullptr;
+      f.b0 = b0;
+      finalize_kernel<<<(unsigned)rows, 256, 0, st>>>(f);
+      CUDA_TRY(cudaGetLastError());
+    }
+  } else {
+    const size_t bytes = (size_t)B * ((size_t)1 << P.n) * 2 * rs;
+    if (!P.relabeled) {
+      CUDA_TRY(cudaMemcpyAsync(state, W + wl.psi, bytes, cudaMemcpyDeviceToDevice, st));
+    } else {
+      const int64_t total = B << P.n;
+      const unsigned blocks = (unsigned)((total + 255) / 256);
+      if (c128)
+        export_kernel<double><<<blocks, 256, 0, st>>>((const Cx<double>*)(W + wl.psi), (Cx<double>*)state, P.n, total, (const int*)DT->layout.p);
+      else
+        export_kernel<float><<<blocks, 256, 0, st>>>((const Cx<float>*)(W + wl.psi), (Cx<float>*)state, P.n, total, (const int*)DT->layout.p);
+      CUDA_TRY(cudaGetLastError());
+    }
+  }
+  return TCX_OK;
+}
+
+}  // namespace
+
+// ================================================================== C ABI
+extern "C" {
+
+const char* tcx_last_error(void) { return g_err.c_str(); }
+const char* tcx_version(void) { return "tcx 0.1 (sm_100a)"; }
+
+tcx_status tcx_circuit_build(int32_t n_qubits, int32_t n_params, const tcx_gate* gates,
+                             int64_t n_gates, const double* matrices, int64_t n_matrix_elems,
+                             tcx_dtype dtype, const tcx_build_opts* opts, tcx_circuit** out) {
+  g_err.clear();
+  if (!out) return fail(TCX_E_INVALID, "null out");
+  *out = nullptr;
+  tcx_circuit* c = new (std::nothrow) tcx_circuit();
+  if (!c) return fail(TCX_E_OOM, "out of host memory");
+  std::string err;
+  tcx_status s;
+  try {
+    s = build_plan(n_qubits, n_params, gates, n_gates, matrices, n_matrix_elems, dtype, opts,
+                   c->plan, err);
+  } catch (const std::bad_alloc&) {
+    s = TCX_E_OOM;
+    err = "out of host memory";
+  }
+  if (s) {
+    delete c;
+    return fail(s, err);
+  }
+  *out = c;
+  return TCX_OK;
+}
+
+tcx_status tcx_pauli_build(int32_t n_qubits, int32_t n_terms, const uint8_t* codes,
+                           const double* weights, tcx_pauli** out) {
+  g_err.clear();
+  if (!out) return fail(TCX_E_INVALID, "null out");
+  *out = nullptr;
+  tcx_pauli* p = new (std::nothrow) tcx_pauli();
+  if (!p) return fail(TCX_E_OOM, "out of host memory");
+  std::string err;
+  tcx_status s = build_pauli(n_qubits, n_terms, codes, weights, p->p, err);
+  if (s) {
+    delete p;
+    return fail(s, err);
+  }
+  *out = p;
+  return TCX_OK;
+}
+
+void tcx_circuit_free(tcx_circuit* c) { delete c; }
+void tcx_pauli_free(tcx_pauli* p) {
+  delete p;
+}
+
+tcx_status tcx_workspace_bytes(const tcx_circuit* circ, const tcx_pauli* pauli, int64_t B,
+                               int32_t mode, size_t* bytes) {
+  g_err.clear();
+  if (!circ || !bytes) return fail(TCX_E_INVALID, "null argument");
+  if (B <= 0) return fail(TCX_E_INVALID, "B must be > 0");
+  Plan& P = const_cast<tcx_circuit*>(circ)->plan;
+  int kind = (mode & TCX_WS_STATE) ? K_STATE : ((mode & TCX_WS_GRAD) ? K_GRAD : K_EXPECT);
+  std::shared_ptr<Binding> Bd;
+  if (kind != K_STATE) {
+    if (!pauli) return fail(TCX_E_INVALID, "null pauli");
+    if (pauli->p.n != P.n) return fail(TCX_E_INVALID, "pauli n_qubits != circuit n_qubits");
+    tcx_status s = binding_for(P, pauli, Bd, nullptr);
+    if (s) return s;
+  }
+  *bytes = ws_layout(P, Bd.get(), B, kind, (mode & TCX_WS_HOST_IO) != 0).total;
+  return TCX_OK;
+}
+
+tcx_status tcx_expect_batch(const tcx_circuit* circ, const tcx_pauli* pauli, const double* theta,
+                            int64_t B, double* E, void* ws, size_t ws_bytes, void* stream) {
+  g_err.clear();
+  if (!circ) return fail(TCX_E_INVALID, "null circuit");
+  return run(const_cast<tcx_circuit*>(circ)->plan, pauli, theta, B, E, nullptr, nullptr, ws,
+             ws_bytes, (cudaStream_t)stream, K_EXPECT, nullptr);
+}
+
+tcx_status tcx_grad_batch(const tcx_circuit* circ, const tcx_pauli* pauli, const double* theta,
+                          int64_t B, double* E, double* grad, void* ws, size_t ws_bytes,
+                          void* stream) {
+  g_err.clear();
+  if (!circ) return fail(TCX_E_INVALID, "null circuit");
+  return run(const_cast<tcx_circuit*>(circ)->plan, pauli, theta, B, E, grad, nullptr, ws,
+             ws_bytes, (cudaStream_t)stream, K_GRAD, nullptr);
+}
+
+tcx_status tcx_state_batch(const tcx_circuit* circ, const double* theta, int64_t B, void* state,
+                           void* ws, size_t ws_bytes, void* stream) {
+  g_err.clear();
+  if (!circ) return fail(TCX_E_INVALID, "null circuit");
+  return run(const_cast<tcx_circuit*>(circ)->plan, nullptr, theta, B, nullptr, nullptr, state,
+             ws, ws_bytes, (cudaStream_t)stream, K_STATE, nullptr);
+}
+
+static tcx_status host_call(const tcx_circuit* circ, const tcx_pauli* pauli, const double* th,
+                            int64_t B, double* E, double* grad, void* ws, size_t ws_bytes,
+                            void* stream, int kind) {
+  g_err.clear();
+  if (!circ || !pauli) return fail(TCX_E_INVALID, "null circuit or pauli");
+  if (B <= 0) return fail(TCX_E_INVALID, "B must be > 0");
+  Plan& P = const_cast<tcx_circuit*>(circ)->plan;
+  if (P.P > 0 && !th) return fail(TCX_E_INVALID, "null theta");
+  if (!E || (kind == K_GRAD && P.P > 0 && !grad)) return fail(TCX_E_INVALID, "null output");
+  std::shared_ptr<Binding> Bd;
+  tcx_status s = binding_for(P, pauli, Bd, nullptr);
+  if (s) return s;
+  WsLayout wl = ws_layout(P, Bd.get(), B, kind, true);
+  if (ws_bytes < wl.total)
+    return fail(TCX_E_INVALID, "workspace too small: need " + std::to_string(wl.total));
+  cudaStream_t st = (cudaStream_t)stream;
+  char* W = (char*)ws;
+  double* dth = (double*)(W + wl.theta);
+  double* dE = (double*)(W + wl.E);
+  double* dG = (double*)(W + wl.grad);
+  if (P.P > 0)
+    CUDA_TRY(cudaMemcpyAsync(dth, th, sizeof(double) * B * P.P, cudaMemcpyHostToDevice, st));
+  s = run(P, pauli, dth, B, dE, dG, nullptr, ws, ws_bytes, st, kind, &wl);
+  if (s) return s;
+  CUDA_TRY(cudaMemcpyAsync(E, dE, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
+  if (kind == K_GRAD && P.P > 0)
+    CUDA_TRY(cudaMemcpyAsync(grad, dG, sizeof(double) * B * P.P, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return TCX_OK;
+}
+
+tcx_status tcx_expect_batch_host(const tcx_circuit* circ, const tcx_pauli* pauli,
+                                 const double* theta_host, int64_t B, double* E_host, void* ws,
+                                 size_t ws_bytes, void* stream) {
+  return host_call(circ, pauli, theta_host, B, E_host, nullptr, ws, ws_bytes, stream, K_EXPECT);
+}
+
+tcx_status tcx_grad_batch_host(const tcx_circuit* circ, const tcx_pauli* pauli,
+                               const double* theta_host, int64_t B, double* E_host,
+                               double* grad_host, void* ws, size_t ws_bytes, void* stream) {
+  return host_call(circ, pauli, theta_host, B, E_host, grad_host, ws, ws_bytes, stream, K_GRAD);
+}
+
+tcx_status tcx_circuit_info(const tcx_circuit* circ, const tcx_pauli* pauli, tcx_plan_info* o) {
+  g_err.clear();
+  if (!circ || !o) return fail(TCX_E_INVALID, "null argument");
+  Plan& P = const_cast<tcx_circuit*>(circ)->plan;
+  std::memset(o, 0, sizeof(*o));
+  o->n_qubits = P.n;
+  o->n_params = P.P;
+  o->dtype = P.dtype;
+  o->tile_bits = P.t;
+  o->reg_bits = P.r;
+  o->coalesce_bits = P.c;
+  o->threads_per_tile = 1 << P.h;
+  o->n_ops = (int)P.ops.size();
+  o->fwd_passes = (int)P.passes.size();
+  o->bwd_passes = (int)P.passes.size();
+  int st = 0;
+  for (auto& p : P.passes) st += p.stage_count;
+  o->stages = st;
+  o->unitary = P.unitary;
+  o->relabeled = P.relabeled;
+  o->tiles_per_state = P.tiles;
+  o->acc_slots = P.acc_total;
+  o->mat_reals = P.mat_total;
+  o->lambda_passes = 0;
+  if (pauli) {
+    std::shared_ptr<Binding> Bd;
+    tcx_status s = binding_for(P, pauli, Bd, nullptr);
+    if (s) return s;
+    o->lambda_passes = (int)Bd->units.size() - 1;
+  }
+  return TCX_OK;
+}
+
+tcx_status tcx_profile_enable(int32_t on) {
+  g_err.clear();
+  g_prof.on = on != 0;
+  return TCX_OK;
+}
+
+tcx_status tcx_profile_read(tcx_kernel_time* out, int32_t cap, int32_t* n) {
+  g_err.clear();
+  if (!n) return fail(TCX_E_INVALID, "null n");
+  int32_t k = 0;
+  for (auto& e : g_prof.log) {
+    float ms = 0.f;
+    cudaEventSynchronize(e.b);
+    cudaEventElapsedTime(&ms, e.a, e.b);
+    if (out && k < cap) {
+      out[k].phase = e.phase;
+      out[k].index = e.index;
+      out[k].ms = ms;
+      out[k].pad = 0.f;
+      out[k].flops = e.flops;
+      out[k].bytes = e.bytes;
+    }
+    ++k;
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
+  g_prof.log.clear();
+  *n = std::min(k, cap);
+  return TCX_OK;
+}
+
+tcx_status tcx_circuit_decode(const tcx_circuit* circ, tcx_gate* out, int64_t cap, int64_t* n) {
+  g_err.clear();
+  if (!circ || !n) return fail(TCX_E_INVALID, "null argument");
+  const Plan& P = circ->plan;
+  *n = (int64_t)P.gates.size();
+  if (out)
+    for (int64_t i = 0; i < std::min<int64_t>(cap, *n); ++i) out[i] = P.gates[i];
+  return TCX_OK;
+}
+
+tcx_status tcx_circuit_layout(const tcx_circuit* circ, int32_t* out) {
+  g_err.clear();
+  if (!circ || !out) return fail(TCX_E_INVALID, "null argument");
+  for (int q = 0; q < circ->plan.n; ++q) out[q] = circ->plan.layout[q];
+  return TCX_OK;
+}
+
+tcx_status tcx_launch_count(const tcx_circuit* circ, const tcx_pauli* pauli, int64_t B,
+                            int32_t want_grad, int32_t* launches) {
+  g_err.clear();
+  if (!circ || !pauli || !launches) return fail(TCX_E_INVALID, "null argument");
+  Plan& P = const_cast<tcx_circuit*>(circ)->plan;
+  std::shared_ptr<Binding> Bd;
+  tcx_status s = binding_for(P, pauli, Bd, nullptr);
+  if (s) return s;
+  const int kind = want_grad ? K_GRAD : K_EXPECT;
+  WsLayout wl = ws_layout(P, Bd.get(), B, kind, false);
+  const int64_t chunks = (B + 65534) / 65535;
+  int64_t per = 0;
+  per += P.mitems.empty() ? 0 : 1;
+  if (wl.mega)
+    per += 1;
+  else
+    per += (int64_t)P.passes.size() + (int64_t)Bd->units.size() - 1 +
+           (want_grad ? (int64_t)P.passes.size() : 0);
+  per += 1;  // finalize
+  *launches = (int32_t)(per * chunks);
+  return TCX_OK;
+}
+
+}  // extern "C"

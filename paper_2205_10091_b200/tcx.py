@@ -1,0 +1,316 @@
+"""Thin Python binding of libtcx.so (include/tcx.h): argument marshalling only.
+
+Every step of the hot path runs in the library's sm_100a kernels.  PyTorch supplies
+device memory and streams.  If the shared library is missing this module raises at
+import time -- there is no CPU fallback (the oracle under oracle/ is test
+infrastructure and is never imported here).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtcx.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libtcx.so not built at {LIB_PATH}; run __graft_entry__.build()")
+_lib = ctypes.CDLL(LIB_PATH)
+
+# tcx_gate_kind (include/tcx.h)
+KIND = {name: i for i, name in enumerate(
+    ("i", "x", "y", "z", "h", "s", "sdg", "t", "tdg", "cnot", "cz", "swap",
+     "rx", "ry", "rz", "rxx", "ryy", "rzz", "u1", "u2"))}
+C64, C128 = 0, 1
+WS_GRAD, WS_HOST_IO, WS_STATE = 1, 2, 4
+STATUS = {0: "OK", 1: "E_INVALID", 2: "E_UNSUPPORTED", 3: "E_OOM", 4: "E_CUDA", 5: "E_NCCL"}
+
+
+class TcxError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"tcx {STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class tcx_gate(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("q0", ctypes.c_int32), ("q1", ctypes.c_int32),
+                ("param", ctypes.c_int32), ("coeff", ctypes.c_double),
+                ("payload", ctypes.c_int64)]
+
+
+class tcx_build_opts(ctypes.Structure):
+    _fields_ = [("tile_bits", ctypes.c_int32), ("reg_bits", ctypes.c_int32),
+                ("coalesce_bits", ctypes.c_int32), ("max_ops_per_pass", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 4)]
+
+
+class tcx_plan_info(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_int32) for f in (
+        "n_qubits", "n_params", "dtype", "tile_bits", "reg_bits", "coalesce_bits",
+        "threads_per_tile", "n_ops", "fwd_passes", "lambda_passes", "bwd_passes", "stages",
+        "unitary", "relabeled")] + [(f, ctypes.c_int64) for f in (
+            "tiles_per_state", "acc_slots", "mat_reals")]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class tcx_kernel_time(ctypes.Structure):
+    _fields_ = [("phase", ctypes.c_int32), ("index", ctypes.c_int32), ("ms", ctypes.c_float),
+                ("pad", ctypes.c_float), ("flops", ctypes.c_double), ("bytes", ctypes.c_double)]
+
+
+PHASES = {0: "materialize", 1: "forward", 2: "lambda", 3: "backward", 4: "finalize", 5: "fused"}
+
+_vp, _i32, _i64, _sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+_dp = ctypes.POINTER(ctypes.c_double)
+_sig = {
+    "tcx_circuit_build": [_i32, _i32, ctypes.POINTER(tcx_gate), _i64, _dp, _i64, _i32,
+                          ctypes.POINTER(tcx_build_opts), ctypes.POINTER(_vp)],
+    "tcx_pauli_build": [_i32, _i32, ctypes.POINTER(ctypes.c_uint8), _dp, ctypes.POINTER(_vp)],
+    "tcx_workspace_bytes": [_vp, _vp, _i64, _i32, ctypes.POINTER(_sz)],
+    "tcx_expect_batch": [_vp, _vp, _vp, _i64, _vp, _vp, _sz, _vp],
+    "tcx_grad_batch": [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp],
+    "tcx_state_batch": [_vp, _vp, _i64, _vp, _vp, _sz, _vp],
+    "tcx_expect_batch_host": [_vp, _vp, _vp, _i64, _vp, _vp, _sz, _vp],
+    "tcx_grad_batch_host": [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp],
+    "tcx_circuit_info": [_vp, _vp, ctypes.POINTER(tcx_plan_info)],
+    "tcx_circuit_decode": [_vp, ctypes.POINTER(tcx_gate), _i64, ctypes.POINTER(_i64)],
+    "tcx_circuit_layout": [_vp, ctypes.POINTER(_i32)],
+    "tcx_launch_count": [_vp, _vp, _i64, _i32, ctypes.POINTER(_i32)],
+    "tcx_profile_enable": [_i32],
+    "tcx_profile_read": [ctypes.POINTER(tcx_kernel_time), _i32, ctypes.POINTER(_i32)],
+}
+for _name, _args in _sig.items():
+    f = getattr(_lib, _name)
+    f.argtypes = _args
+    f.restype = ctypes.c_int
+_lib.tcx_circuit_free.argtypes = [_vp]
+_lib.tcx_circuit_free.restype = None
+_lib.tcx_pauli_free.argtypes = [_vp]
+_lib.tcx_pauli_free.restype = None
+_lib.tcx_last_error.restype = ctypes.c_char_p
+_lib.tcx_version.restype = ctypes.c_char_p
+
+EXPORTS = list(_sig) + ["tcx_circuit_free", "tcx_pauli_free", "tcx_last_error", "tcx_version"]
+
+
+def _check(rc):
+    if rc != 0:
+        raise TcxError(rc, _lib.tcx_last_error().decode())
+
+
+def last_error() -> str:
+    return _lib.tcx_last_error().decode()
+
+
+def version() -> str:
+    return _lib.tcx_version().decode()
+
+
+def gate_array(names, q0, q1, param, coeff, moff):
+    G = len(names)
+    arr = (tcx_gate * max(G, 1))()
+    for i in range(G):
+        arr[i].kind = KIND[names[i]]
+        arr[i].q0 = int(q0[i])
+        arr[i].q1 = int(q1[i])
+        arr[i].param = int(param[i])
+        arr[i].coeff = float(coeff[i])
+        arr[i].payload = int(moff[i])
+    return arr
+
+
+class Circuit:
+    """tcx_circuit_build over a gate list (workloads.Circuit or raw arrays)."""
+
+    def __init__(self, circ, dtype: str = "c64", tile_bits: int = 0, reg_bits: int = 0,
+                 coalesce_bits: int = 0, max_ops_per_pass: int = 0, gates=None):
+        names, q0, q1, param, coeff, moff, mats = circ.arrays()
+        self.n = circ.n
+        self.P = circ.n_params
+        self.dtype = dtype
+        self._gates = gates if gates is not None else gate_array(names, q0, q1, param, coeff, moff)
+        self.G = len(names)
+        mats = np.ascontiguousarray(mats, dtype=np.float64)
+        if mats.size == 0:
+            mats = np.zeros(2)
+        self._mats = mats
+        opts = tcx_build_opts(tile_bits, reg_bits, coalesce_bits, max_ops_per_pass)
+        h = _vp()
+        _check(_lib.tcx_circuit_build(self.n, self.P, self._gates, self.G,
+                                      mats.ctypes.data_as(_dp), mats.size // 2,
+                                      C128 if dtype == "c128" else C64, ctypes.byref(opts),
+                                      ctypes.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            _lib.tcx_circuit_free(self.h)
+            self.h = None
+
+    def info(self, pauli: Optional["Pauli"] = None) -> dict:
+        out = tcx_plan_info()
+        _check(_lib.tcx_circuit_info(self.h, pauli.h if pauli else None, ctypes.byref(out)))
+        return out.as_dict()
+
+    def decode(self):
+        n = _i64()
+        _check(_lib.tcx_circuit_decode(self.h, None, 0, ctypes.byref(n)))
+        arr = (tcx_gate * max(n.value, 1))()
+        _check(_lib.tcx_circuit_decode(self.h, arr, n.value, ctypes.byref(n)))
+        return [arr[i] for i in range(n.value)]
+
+    def layout(self):
+        arr = (_i32 * self.n)()
+        _check(_lib.tcx_circuit_layout(self.h, arr))
+        return list(arr)
+
+    def workspace_bytes(self, pauli, B: int, mode: int) -> int:
+        out = _sz()
+        _check(_lib.tcx_workspace_bytes(self.h, pauli.h if pauli else None, B, mode,
+                                        ctypes.byref(out)))
+        return out.value
+
+    def launch_count(self, pauli, B: int, grad: bool) -> int:
+        out = _i32()
+        _check(_lib.tcx_launch_count(self.h, pauli.h, B, int(grad), ctypes.byref(out)))
+        return out.value
+
+
+class Pauli:
+    """tcx_pauli_build over integer structures and real weights."""
+
+    def __init__(self, H):
+        self.n = H.n
+        self.codes = np.ascontiguousarray(H.codes, dtype=np.uint8)
+        self.weights = np.ascontiguousarray(H.weights, dtype=np.float64)
+        h = _vp()
+        _check(_lib.tcx_pauli_build(self.n, len(self.weights),
+                                    self.codes.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)),
+                                    self.weights.ctypes.data_as(_dp), ctypes.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            _lib.tcx_pauli_free(self.h)
+            self.h = None
+
+
+# ----------------------------------------------------------------- torch side
+def _torch():
+    import torch
+    return torch
+
+
+class Workspace:
+    """Caches one device workspace per (circuit, pauli, B, mode)."""
+
+    def __init__(self):
+        self._buf = {}
+
+    def get(self, circ, pauli, B, mode, device):
+        torch = _torch()
+        key = (id(circ), id(pauli) if pauli else 0, B, mode, str(device))
+        need = circ.workspace_bytes(pauli, B, mode)
+        buf = self._buf.get(key)
+        if buf is None or buf.numel() < need:
+            buf = torch.empty(max(need, 16), dtype=torch.uint8, device=device)
+            self._buf[key] = buf
+        return buf, need
+
+    def clear(self):
+        self._buf.clear()
+
+
+_default_ws = Workspace()
+
+
+def _stream_ptr(stream):
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def expect_batch(circ: Circuit, pauli: Pauli, theta, stream=None, ws: Workspace = None):
+    """E[b] for theta [B, P] float64 on a CUDA device (tcx_expect_batch)."""
+    torch = _torch()
+    theta = theta.contiguous()
+    assert theta.dtype == torch.float64 and theta.is_cuda
+    B = theta.shape[0]
+    E = torch.empty(B, dtype=torch.float64, device=theta.device)
+    buf, need = (ws or _default_ws).get(circ, pauli, B, 0, theta.device)
+    _check(_lib.tcx_expect_batch(circ.h, pauli.h, ctypes.c_void_p(theta.data_ptr()), B,
+                                 ctypes.c_void_p(E.data_ptr()), ctypes.c_void_p(buf.data_ptr()),
+                                 buf.numel(), _stream_ptr(stream)))
+    return E
+
+
+def grad_batch(circ: Circuit, pauli: Pauli, theta, stream=None, ws: Workspace = None, out=None):
+    """(E [B], grad [B, P]) per row (tcx_grad_batch; PAPER.md:1121-1139 batched VQE)."""
+    torch = _torch()
+    theta = theta.contiguous()
+    assert theta.dtype == torch.float64 and theta.is_cuda
+    B = theta.shape[0]
+    if out is None:
+        E = torch.empty(B, dtype=torch.float64, device=theta.device)
+        G = torch.empty(B, max(circ.P, 1), dtype=torch.float64, device=theta.device)
+    else:
+        E, G = out
+    buf, need = (ws or _default_ws).get(circ, pauli, B, WS_GRAD, theta.device)
+    _check(_lib.tcx_grad_batch(circ.h, pauli.h, ctypes.c_void_p(theta.data_ptr()), B,
+                               ctypes.c_void_p(E.data_ptr()), ctypes.c_void_p(G.data_ptr()),
+                               ctypes.c_void_p(buf.data_ptr()), buf.numel(),
+                               _stream_ptr(stream)))
+    return E, G[:, :circ.P]
+
+
+def state_batch(circ: Circuit, theta, stream=None, ws: Workspace = None):
+    """psi(theta_b) [B, 2^n] complex64/complex128, paper index order."""
+    torch = _torch()
+    theta = theta.contiguous()
+    B = theta.shape[0]
+    cd = torch.complex128 if circ.dtype == "c128" else torch.complex64
+    out = torch.empty(B, 1 << circ.n, dtype=cd, device=theta.device)
+    buf, need = (ws or _default_ws).get(circ, None, B, WS_STATE, theta.device)
+    _check(_lib.tcx_state_batch(circ.h, ctypes.c_void_p(theta.data_ptr()), B,
+                                ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(buf.data_ptr()),
+                                buf.numel(), _stream_ptr(stream)))
+    return out
+
+
+def grad_batch_host(circ: Circuit, pauli: Pauli, theta_host: np.ndarray, E_host=None,
+                    grad_host=None, stream=None, ws: Workspace = None, device=None):
+    """End-to-end call with HOST buffers (tcx_grad_batch_host): H2D theta, kernels,
+    D2H E/grad, stream synchronize.  Pinned host arrays recommended."""
+    torch = _torch()
+    B = theta_host.shape[0]
+    if E_host is None:
+        E_host = np.empty(B, dtype=np.float64)
+    if grad_host is None:
+        grad_host = np.empty((B, max(circ.P, 1)), dtype=np.float64)
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    buf, need = (ws or _default_ws).get(circ, pauli, B, WS_GRAD | WS_HOST_IO, dev)
+    _check(_lib.tcx_grad_batch_host(circ.h, pauli.h, ctypes.c_void_p(theta_host.ctypes.data), B,
+                                    ctypes.c_void_p(E_host.ctypes.data),
+                                    ctypes.c_void_p(grad_host.ctypes.data),
+                                    ctypes.c_void_p(buf.data_ptr()), buf.numel(),
+                                    _stream_ptr(stream)))
+    return E_host, grad_host[:, :circ.P]
+
+
+def profile_enable(on: bool = True):
+    """Bracket every kernel of the next compute calls on this thread with CUDA events."""
+    _check(_lib.tcx_profile_enable(int(on)))
+
+
+def profile_read(cap: int = 1 << 16):
+    """[(phase, index, ms, flops, bytes)] of the recorded launches; clears the log."""
+    arr = (tcx_kernel_time * cap)()
+    n = _i32()
+    _check(_lib.tcx_profile_read(arr, cap, ctypes.byref(n)))
+    return [(PHASES[arr[i].phase], arr[i].index, arr[i].ms, arr[i].flops, arr[i].bytes)
+            for i in range(n.value)]

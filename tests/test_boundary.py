@@ -1,0 +1,147 @@
+"""CPU tests of the C-ABI library: it loads, exports every symbol include/tcx.h declares,
+validates gate lists bit-exactly, and its compute entries refuse to run without a GPU
+(there is no CPU fallback).  No compute calls here."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import workloads as W
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def tcx():
+    from paper_2205_10091_b200 import tcx as m
+    return m
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "tcx.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(tcx_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(tcx):
+    syms = header_symbols()
+    assert len(syms) >= 15
+    lib = ctypes.CDLL(tcx.LIB_PATH)
+    for s in syms:
+        assert hasattr(lib, s), f"libtcx.so does not export {s}"
+    assert set(syms) == set(tcx.EXPORTS)
+
+
+def test_sm100a_cubin_only(tcx):
+    """The library carries sm_100a SASS (no PTX-JIT / other-arch fallback)."""
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", tcx.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert "sm_90" not in out and "sm_80" not in out
+
+
+def test_decode_roundtrip_bit_exact(tcx):
+    c = W.random_circuit(7, 200, 3, n_params=9)
+    C = tcx.Circuit(c, "c64")
+    dec = C.decode()
+    names, q0, q1, param, coeff, moff, _ = c.arrays()
+    assert len(dec) == len(names)
+    for i, g in enumerate(dec):
+        assert g.kind == tcx.KIND[names[i]] and g.q0 == q0[i] and g.q1 == q1[i]
+        assert g.param == param[i] and g.payload == moff[i]
+        assert np.float64(g.coeff).tobytes() == np.float64(coeff[i]).tobytes()
+
+
+@pytest.mark.parametrize("bad,idx", [
+    (lambda c: c.add("cnot", 1, 1), "q0 == q1"),
+    (lambda c: c.add("rx", 5, param=0, coeff=1.0), "q0 out of range"),
+    (lambda c: c.add("ry", 0, param=7, coeff=1.0), "param out of range"),
+    (lambda c: c.add("h", 0, param=1), "param must be -1"),
+    (lambda c: c.add("cz", 0, 9), "q1 out of range"),
+    (lambda c: c.add("x", 0, 1), "q1 must be -1"),
+])
+def test_validation_names_gate(tcx, bad, idx):
+    c = W.Circuit(5, 3).add("h", 0).add("h", 1)
+    bad(c)
+    with pytest.raises(tcx.TcxError) as e:
+        tcx.Circuit(c, "c64")
+    assert e.value.code == 1
+    assert "gate 2" in str(e.value) and idx in str(e.value)
+
+
+def test_payload_validation(tcx):
+    c = W.Circuit(2, 0).add("u1", 0, matrix=np.eye(2))
+    c.gates[0].matrix = None  # payload offset -1 for a u1 gate
+    with pytest.raises(tcx.TcxError):
+        tcx.Circuit(c, "c64")
+
+
+def test_pauli_validation(tcx):
+    H = W.PauliSum(3, np.array([[0, 4, 1]], np.uint8), np.array([1.0]))
+    with pytest.raises(tcx.TcxError) as e:
+        tcx.Pauli(H)
+    assert "term 0" in str(e.value)
+
+
+def test_layout_swap_relabel(tcx):
+    """SWAP gates become qubit relabels (bit-exact permutation of index bits)."""
+    n = 5
+    c = W.Circuit(n, 0).add("swap", 0, 3).add("swap", 3, 4).add("h", 2)
+    C = tcx.Circuit(c, "c64")
+    pos = [n - 1 - q for q in range(n)]
+    pos[0], pos[3] = pos[3], pos[0]
+    pos[3], pos[4] = pos[4], pos[3]
+    assert C.layout() == pos
+    assert C.info()["relabeled"] == 1
+    assert tcx.Circuit(W.hea(5, 1), "c64").layout() == [n - 1 - q for q in range(n)]
+
+
+def test_plan_covers_configs(tcx):
+    """Every BASELINE config compiles; passes/stages are sane; cfg1 is one fused pass."""
+    infos = {}
+    for idx in range(5):
+        name, c, H, th, dt = W.config(idx, B=1)
+        C = tcx.Circuit(c, dt)
+        infos[idx] = C.info(tcx.Pauli(H))
+        assert infos[idx]["fwd_passes"] >= 1
+    assert infos[0]["fwd_passes"] == 1 and infos[0]["lambda_passes"] == 0
+    assert infos[1]["tiles_per_state"] == 2 ** (20 - 12)
+    # fused: far fewer passes than gates
+    assert infos[1]["fwd_passes"] * 20 < len(W.hea(20, 10).gates)
+
+
+def test_unfused_option(tcx):
+    c = W.hea(8, 2)
+    C1 = tcx.Circuit(c, "c64", tile_bits=6, max_ops_per_pass=1)
+    C2 = tcx.Circuit(c, "c64", tile_bits=6)
+    assert C1.info()["fwd_passes"] == C1.info()["n_ops"]
+    assert C2.info()["fwd_passes"] < C1.info()["fwd_passes"]
+
+
+def test_workspace_bytes_monotone(tcx):
+    name, c, H, th, dt = W.config(1, B=1)
+    C, P = tcx.Circuit(c, dt), tcx.Pauli(H)
+    b1 = C.workspace_bytes(P, 1, tcx.WS_GRAD)
+    b8 = C.workspace_bytes(P, 8, tcx.WS_GRAD)
+    e8 = C.workspace_bytes(P, 8, 0)
+    assert b8 > b1 and b8 > e8 >= 8 * (1 << 20) * 8
+
+
+def test_no_cpu_fallback(tcx):
+    """Without a CUDA device the compute entries fail loudly (TCX_E_CUDA)."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    c = W.hea(4, 1)
+    C, P = tcx.Circuit(c, "c64"), tcx.Pauli(W.tfim_zz_x(4))
+    buf = ctypes.create_string_buffer(1 << 16)
+    th = np.zeros(c.n_params)
+    E = np.zeros(1)
+    g = np.zeros(c.n_params)
+    rc = tcx._lib.tcx_grad_batch(C.h, P.h, ctypes.c_void_p(th.ctypes.data), 1,
+                                 ctypes.c_void_p(E.ctypes.data), ctypes.c_void_p(g.ctypes.data),
+                                 ctypes.cast(buf, ctypes.c_void_p), len(buf), None)
+    assert rc == 4, tcx.last_error()
+    assert "no CUDA device" in tcx.last_error()

@@ -1,0 +1,269 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by element.
+
+Tolerances: SURVEY §8c C9 reading (tests/helpers.py): |dE| <= tol*|H|_1,
+|dgrad_p| <= tol*|H|_1*sum_{g in p}|coeff_g|, normwise grad <= tol where the gradient is
+not tiny; tol = 1e-5 (complex64) / 1e-11 (complex128).  States: absolute per amplitude.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import workloads as W
+from helpers import check_E, check_grad, state_tol
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def tc():
+    import torch
+    from paper_2205_10091_b200 import tcx
+    assert torch.cuda.is_available()
+    return tcx
+
+
+def _th(theta):
+    import torch
+    return torch.as_tensor(np.ascontiguousarray(theta, dtype=np.float64)).cuda()
+
+
+def run_grad(tc, c, H, theta, dtype, **opts):
+    C, P = tc.Circuit(c, dtype, **opts), tc.Pauli(H)
+    E, G = tc.grad_batch(C, P, _th(theta))
+    return E.cpu().numpy(), G.cpu().numpy(), C
+
+
+def oracle_grad(c, H, theta):
+    return orc.value_grad_batch(c, H, theta, nthreads=os.cpu_count() or 1)
+
+
+# ------------------------------------------------------------------- states
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 11])
+def test_state_random_all_kinds_single_tile(tc, dtype, n):
+    c = W.random_circuit(n, 60, 1000 + n, n_params=5)
+    th = W.thetas(3, 5, n)
+    C = tc.Circuit(c, dtype)
+    psi = tc.state_batch(C, _th(th)).cpu().numpy()
+    for b in range(3):
+        ref = orc.state(c, th[b])
+        err = np.abs(psi[b] - ref).max()
+        assert err <= state_tol(dtype, len(c.gates)), f"row {b}: {err}"
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("n,t", [(10, 5), (13, 7), (14, 9), (15, 8)])
+def test_state_multi_pass(tc, dtype, n, t):
+    """Several windows and tiles per state (small tile_bits forces many passes)."""
+    c = W.random_circuit(n, 120, 2000 + n, n_params=6)
+    th = W.thetas(2, 6, n)
+    C = tc.Circuit(c, dtype, tile_bits=t, coalesce_bits=2)
+    info = C.info()
+    assert info["tiles_per_state"] > 1 and info["fwd_passes"] > 1
+    psi = tc.state_batch(C, _th(th)).cpu().numpy()
+    for b in range(2):
+        ref = orc.state(c, th[b])
+        assert np.abs(psi[b] - ref).max() <= state_tol(dtype, len(c.gates))
+
+
+def test_fig2_golden_on_gpu(tc):
+    """PAPER.md:257-272 Fig. 2 amplitudes through the CUDA path."""
+    c = W.Circuit(2, 0).add("h", 0).add("cnot", 0, 1).add("rx", 1, param=-1, coeff=0.2)
+    g = np.loadtxt(os.path.join(GOLD, "fig2_state.txt"))
+    psi = tc.state_batch(tc.Circuit(c, "c128"), _th(np.zeros((1, 0)))).cpu().numpy()[0]
+    np.testing.assert_allclose(psi, g[:, 1] + 1j * g[:, 2], atol=1e-15)
+
+
+def test_batched_vqe_golden_on_gpu(tc):
+    """PAPER.md:1121-1139 batched VQE example through tcx_grad_batch."""
+    c = W.Circuit(2, 2).add("rx", 0, param=0, coeff=1.0).add("cnot", 0, 1).add("rx", 1, param=1, coeff=1.0)
+    H = W.pauli_sum(2, [({0: "Z", 1: "Z"}, 1.0)])
+    g = np.loadtxt(os.path.join(GOLD, "batched_vqe.txt"))
+    for dtype, tol in (("c128", 1e-14), ("c64", 1e-6)):
+        E, G, _ = run_grad(tc, c, H, np.array([[0.1, 0.2], [0.3, 0.4]]), dtype)
+        np.testing.assert_allclose(E, g[:, 1], atol=tol)
+        np.testing.assert_allclose(G, g[:, 2:], atol=tol)
+
+
+# -------------------------------------------------------------- E + gradient
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("seed", range(4))
+def test_grad_random_circuits(tc, dtype, seed):
+    n = 3 + seed * 2
+    c = W.random_circuit(n, 80, 3000 + seed, n_params=7, with_payload=True)
+    H = W.random_pauli_sum(n, 10, seed)
+    th = W.thetas(5, 7, seed)
+    E, G, _ = run_grad(tc, c, H, th, dtype)
+    Er, Gr = oracle_grad(c, H, th)
+    check_E(E, Er, H, dtype, "E")
+    check_grad(G, Gr, H, c, dtype, "grad")
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("n,t,seed", [(12, 7, 0), (14, 8, 1), (13, 6, 2)])
+def test_grad_multi_pass_random(tc, dtype, n, t, seed):
+    """Multi-pass forward, extra lambda passes, multi-pass backward, several tiles."""
+    c = W.random_circuit(n, 90, 4000 + seed, n_params=6)
+    H = W.random_pauli_sum(n, 12, 40 + seed)
+    th = W.thetas(3, 6, seed)
+    E, G, C = run_grad(tc, c, H, th, dtype, tile_bits=t, coalesce_bits=2)
+    info = C.info(tc.Pauli(H))
+    assert info["fwd_passes"] > 1
+    Er, Gr = oracle_grad(c, H, th)
+    check_E(E, Er, H, dtype, "E")
+    check_grad(G, Gr, H, c, dtype, "grad")
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_grad_hea_heisenberg_multi_tile(tc, dtype):
+    n, d = 14, 4
+    c, H = W.hea(n, d), W.heisenberg(n)
+    th = W.thetas(4, c.n_params, 7)
+    E, G, C = run_grad(tc, c, H, th, dtype, tile_bits=10)
+    info = C.info(tc.Pauli(H))
+    assert info["fwd_passes"] > 1 and info["lambda_passes"] >= 1
+    Er, Gr = oracle_grad(c, H, th)
+    check_E(E, Er, H, dtype)
+    check_grad(G, Gr, H, c, dtype)
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_expect_matches_grad_E(tc, dtype):
+    c, H = W.hea(12, 3), W.tfim_zz_x(12)
+    th = W.thetas(6, c.n_params, 3)
+    C, P = tc.Circuit(c, dtype, tile_bits=9), tc.Pauli(H)
+    E1 = tc.expect_batch(C, P, _th(th)).cpu().numpy()
+    E2, _ = tc.grad_batch(C, P, _th(th))
+    Er = orc.expect_batch(c, H, th)
+    check_E(E1, Er, H, dtype)
+    np.testing.assert_allclose(E1, E2.cpu().numpy(), rtol=0, atol=10 * {"c64": 1e-6, "c128": 1e-14}[dtype] * H.l1)
+
+
+def test_cfg1_full_vs_oracle(tc):
+    """BASELINE configs[0] at full size: n=10 HEA d=4, TFIM, B=16, complex128."""
+    name, c, H, th, dt = W.config(0)
+    E, G, _ = run_grad(tc, c, H, th, dt)
+    Er, Gr = oracle_grad(c, H, th)
+    check_E(E, Er, H, dt)
+    check_grad(G, Gr, H, c, dt)
+
+
+def test_qaoa_small_vs_oracle(tc):
+    n = 12
+    edges = W.random_regular_graph(n, 3, 3)
+    c, H = W.qaoa_maxcut(n, 3, edges), W.maxcut_cost(n, edges)
+    th = W.qaoa_thetas(8, 3, 3)
+    for dtype in ("c64", "c128"):
+        E, G, _ = run_grad(tc, c, H, th, dtype, tile_bits=8)
+        Er, Gr = oracle_grad(c, H, th)
+        check_E(E, Er, H, dtype)
+        check_grad(G, Gr, H, c, dtype)
+
+
+# ------------------------------------------------------------ closed forms
+def test_qaoa_ring_closed_form_n24(tc):
+    """North-star pin at the cfg3 size: p=1 ring <C> = n(1/2 + 1/4 sin4b sin2g)."""
+    n = 24
+    edges = W.ring_graph(n)
+    c, H = W.qaoa_maxcut(n, 1, edges), W.maxcut_cost(n, edges)
+    th = W.qaoa_thetas(4, 1, 11)
+    E, G, _ = run_grad(tc, c, H, th, "c64")
+    g_, b_ = th[:, 0], th[:, 1]
+    want = n * (0.5 + 0.25 * np.sin(4 * b_) * np.sin(2 * g_))
+    dg = n * 0.5 * np.sin(4 * b_) * np.cos(2 * g_)
+    db = n * np.cos(4 * b_) * np.sin(2 * g_)
+    check_E(E, want, H, "c64")
+    np.testing.assert_allclose(G[:, 0], dg, atol=1e-5 * H.l1 * 36)
+    np.testing.assert_allclose(G[:, 1], db, atol=1e-5 * H.l1 * 48)
+
+
+def test_ghz_ry_closed_form_n24(tc):
+    """GHZ then Ry(t_i) on TFIM(ZZ+X): E = sum cos t_i cos t_i+1 (large-n pin)."""
+    n = 24
+    c = W.Circuit(n, n).add("h", 0)
+    for q in range(n - 1):
+        c.add("cnot", q, q + 1)
+    for q in range(n):
+        c.add("ry", q, param=q, coeff=1.0)
+    H = W.tfim_zz_x(n)
+    th = W.thetas(2, n, 5)
+    E, G, _ = run_grad(tc, c, H, th, "c64")
+    ct, st = np.cos(th), np.sin(th)
+    want = np.sum(ct[:, :-1] * ct[:, 1:], axis=1)
+    nb = np.zeros_like(th)
+    nb[:, 1:] += ct[:, :-1]
+    nb[:, :-1] += ct[:, 1:]
+    check_E(E, want, H, "c64")
+    np.testing.assert_allclose(G, -st * nb, atol=1e-5 * H.l1)
+
+
+def test_hea_zero_theta_n20(tc):
+    c, H = W.hea(20, 10), W.heisenberg(20)
+    E, G, _ = run_grad(tc, c, H, np.zeros((2, c.n_params)), "c64")
+    np.testing.assert_allclose(E, 19.0, atol=1e-5 * H.l1)
+
+
+# ------------------------------------------------------------ full-size cfg2
+@pytest.mark.slow
+def test_cfg2_full_batch_sampled_rows(tc):
+    """configs[1] at full size in the bench launch configuration (B=1024, c64); two
+    sampled rows checked against the oracle one by one, all rows checked for the
+    theta-independent invariant |E| <= |H|_1 and finiteness."""
+    name, c, H, th, dt = W.config(1)
+    E, G, _ = run_grad(tc, c, H, th, dt)
+    assert np.isfinite(E).all() and np.isfinite(G).all()
+    assert (np.abs(E) <= H.l1).all()
+    rows = [0, 777]
+    Er, Gr = orc.value_grad_batch(c, H, th[rows], nthreads=2)
+    check_E(E[rows], Er, H, dt, "cfg2 E")
+    check_grad(G[rows], Gr, H, c, dt, "cfg2 grad")
+
+
+# --------------------------------------------------------------- semantics
+def test_deterministic_and_batch_invariant(tc):
+    c, H = W.hea(13, 3), W.heisenberg(13)
+    th = W.thetas(6, c.n_params, 1)
+    E1, G1, _ = run_grad(tc, c, H, th, "c64", tile_bits=9)
+    E2, G2, _ = run_grad(tc, c, H, th, "c64", tile_bits=9)
+    assert np.array_equal(E1, E2) and np.array_equal(G1, G2)
+    E3, G3, _ = run_grad(tc, c, H, th[2:3], "c64", tile_bits=9)
+    assert np.array_equal(E3[0], E1[2]) and np.array_equal(G3[0], G1[2])
+
+
+def test_host_e2e_matches_device(tc):
+    c, H = W.hea(10, 2), W.tfim_zz_x(10)
+    th = W.thetas(4, c.n_params, 2)
+    C, P = tc.Circuit(c, "c64"), tc.Pauli(H)
+    E, G = tc.grad_batch(C, P, _th(th))
+    Eh, Gh = tc.grad_batch_host(C, P, np.ascontiguousarray(th))
+    assert np.array_equal(E.cpu().numpy(), Eh) and np.array_equal(G.cpu().numpy(), Gh)
+
+
+def test_nonunitary_grad_unsupported(tc):
+    c = W.Circuit(2, 1).add("u1", 0, matrix=np.array([[1, 2], [2, 3]])).add("rx", 1, param=0, coeff=1.0)
+    H = W.pauli_sum(2, [({0: "Z"}, 1.0)])
+    C, P = tc.Circuit(c, "c128"), tc.Pauli(H)
+    with pytest.raises(tc.TcxError) as e:
+        tc.grad_batch(C, P, _th(np.zeros((1, 1))))
+    assert e.value.code == 2
+    # forward with a non-unitary payload is allowed
+    E = tc.expect_batch(C, P, _th(np.zeros((1, 1)))).cpu().numpy()
+    assert abs(E[0] - orc.expect_batch(c, H, np.zeros((1, 1)))[0]) < 1e-12
+
+
+def test_workspace_too_small(tc):
+    import ctypes
+    import torch
+    c, H = W.hea(6, 1), W.tfim_zz_x(6)
+    C, P = tc.Circuit(c, "c64"), tc.Pauli(H)
+    th = _th(np.zeros((1, c.n_params)))
+    E = torch.empty(1, dtype=torch.float64, device="cuda")
+    G = torch.empty(1, c.n_params, dtype=torch.float64, device="cuda")
+    buf = torch.empty(64, dtype=torch.uint8, device="cuda")
+    rc = tc._lib.tcx_grad_batch(C.h, P.h, ctypes.c_void_p(th.data_ptr()), 1, ctypes.c_void_p(E.data_ptr()),
+                                ctypes.c_void_p(G.data_ptr()), ctypes.c_void_p(buf.data_ptr()), 64, None)
+    assert rc == 1 and "workspace too small" in tc.last_error()
