@@ -184,12 +184,11 @@ def main():
     stream = torch.cuda.current_stream(dev)
     ws = tcx.Workspace()
 
+    from paper_2205_10091_b200.dist import allreduce_loss_grad
+
     def step():
         tcx.grad_batch(C, P, th, stream=stream, ws=ws, out=(E, G))
-        red[0] = E.sum()
-        red[1:] = G[:, :circ.n_params].sum(0)
-        if world > 1:
-            dist.all_reduce(red)
+        allreduce_loss_grad(E, G[:, :circ.n_params], out=red)
 
     for _ in range(args.warmup):
         step()

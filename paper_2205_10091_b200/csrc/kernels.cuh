@@ -183,6 +183,21 @@ __device__ __forceinline__ void apply_u1(Cx<Real>* v, const Real (&m)[8]) {
     v[j1].y = m[4] * p.y + m[5] * p.x + m[6] * q.y + m[7] * q.x;
   }
 }
+// U^dagger on slot K from the same m (conj-transpose folded into operand signs).
+template <int RB, int K, typename Real>
+__device__ __forceinline__ void apply_u1_dag(Cx<Real>* v, const Real (&m)[8]) {
+#pragma unroll
+  for (int j = 0; j < (1 << RB); ++j) {
+    if (j & (1 << K)) continue;
+    const int j1 = j | (1 << K);
+    const Cx<Real> p = v[j], q = v[j1];
+    // out0 = conj(u00) p + conj(u10) q ; out1 = conj(u01) p + conj(u11) q
+    v[j].x = m[0] * p.x + m[1] * p.y + m[4] * q.x + m[5] * q.y;
+    v[j].y = m[0] * p.y - m[1] * p.x + m[4] * q.y - m[5] * q.x;
+    v[j1].x = m[2] * p.x + m[3] * p.y + m[6] * q.x + m[7] * q.y;
+    v[j1].y = m[2] * p.y - m[3] * p.x + m[6] * q.y - m[7] * q.x;
+  }
+}
 // R'_ab += psi_a conj(lambda_b) over the pairs of slot K (a, b = value of the bit).
 template <int RB, int K, typename Real>
 __device__ __forceinline__ void accum_r(const Cx<Real>* v, const Cx<Real>* l, Real (&r)[8]) {
@@ -191,30 +206,70 @@ __device__ __forceinline__ void accum_r(const Cx<Real>* v, const Cx<Real>* l, Re
     if (j & (1 << K)) continue;
     const int j1 = j | (1 << K);
     const Cx<Real> p0 = v[j], p1 = v[j1], l0 = l[j], l1 = l[j1];
-    r[0] += p0.x * l0.x + p0.y * l0.y;
-    r[1] += p0.y * l0.x - p0.x * l0.y;
-    r[2] += p0.x * l1.x + p0.y * l1.y;
-    r[3] += p0.y * l1.x - p0.x * l1.y;
-    r[4] += p1.x * l0.x + p1.y * l0.y;
-    r[5] += p1.y * l0.x - p1.x * l0.y;
-    r[6] += p1.x * l1.x + p1.y * l1.y;
-    r[7] += p1.y * l1.x - p1.x * l1.y;
+    r[0] = fma(p0.x, l0.x, fma(p0.y, l0.y, r[0]));
+    r[1] = fma(p0.y, l0.x, fma(-p0.x, l0.y, r[1]));
+    r[2] = fma(p0.x, l1.x, fma(p0.y, l1.y, r[2]));
+    r[3] = fma(p0.y, l1.x, fma(-p0.x, l1.y, r[3]));
+    r[4] = fma(p1.x, l0.x, fma(p1.y, l0.y, r[4]));
+    r[5] = fma(p1.y, l0.x, fma(-p1.x, l0.y, r[5]));
+    r[6] = fma(p1.x, l1.x, fma(p1.y, l1.y, r[6]));
+    r[7] = fma(p1.y, l1.x, fma(-p1.x, l1.y, r[7]));
   }
 }
-// CNOT with target slot KT; control = register slot kc (kc < RB) or the thread/tile
-// constant `cext` (kc == 0xFF).  Self-inverse.
+// CNOT with target slot KT and control register slot KC: register swaps.
+template <int RB, int KT, int KC, typename Real>
+__device__ __forceinline__ void apply_cx_rr(Cx<Real>* v) {
+#pragma unroll
+  for (int j = 0; j < (1 << RB); ++j) {
+    if ((j & (1 << KT)) || !(j & (1 << KC))) continue;
+    const int j1 = j | (1 << KT);
+    const Cx<Real> p = v[j];
+    v[j] = v[j1];
+    v[j1] = p;
+  }
+}
+// CNOT with target slot KT and a control bit outside the registers (thread/tile bit
+// `c`): warp-uniform controls branch, lane-varying ones select.  Self-inverse.
 template <int RB, int KT, typename Real>
-__device__ __forceinline__ void apply_cx(Cx<Real>* v, int kc, bool cext) {
+__device__ __forceinline__ void apply_cx_ext(Cx<Real>* v, bool c, bool uniform) {
+  if (uniform) {
+    if (c) {
+#pragma unroll
+      for (int j = 0; j < (1 << RB); ++j) {
+        if (j & (1 << KT)) continue;
+        const Cx<Real> p = v[j];
+        v[j] = v[j | (1 << KT)];
+        v[j | (1 << KT)] = p;
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int j = 0; j < (1 << RB); ++j) {
     if (j & (1 << KT)) continue;
     const int j1 = j | (1 << KT);
-    const bool c = kc < RB ? ((j >> kc) & 1) : cext;
     const Cx<Real> p = v[j], q = v[j1];
     v[j].x = c ? q.x : p.x;
     v[j].y = c ? q.y : p.y;
     v[j1].x = c ? p.x : q.x;
     v[j1].y = c ? p.y : q.y;
+  }
+}
+template <int RB, typename Real>
+__device__ __forceinline__ void op_cx(const KOp& o, Cx<Real>* v, uint64_t g) {
+  if (o.b == kExtCtrl) {
+    const bool c = (g >> o.cbit) & 1;
+    const bool uni = o.nterm != 0;  // plan: control is an outer or warp bit
+    dispatch_slot<RB>(o.a, [&](auto KT) { apply_cx_ext<RB, decltype(KT)::value>(v, c, uni); });
+  } else {
+    if constexpr (RB >= 2) {
+      dispatch_slot<RB>(o.a, [&](auto KT) {
+        dispatch_slot<RB>(o.b, [&](auto KC) {
+          if constexpr (decltype(KT)::value != decltype(KC)::value)
+            apply_cx_rr<RB, decltype(KT)::value, decltype(KC)::value>(v);
+        });
+      });
+    }
   }
 }
 
@@ -324,9 +379,7 @@ __device__ __forceinline__ void op_fwd(const KOp& o, Cx<Real>* v, const Map<RB>&
     for (int i = 0; i < 8; ++i) m[i] = mats[o.mat + i];
     dispatch_slot<RB>(o.a, [&](auto K) { apply_u1<RB, decltype(K)::value>(v, m); });
   } else if (o.type == OP_CX) {
-    const bool c = (mp.g >> o.cbit) & 1;
-    const int kc = o.b == kExtCtrl ? 0xFF : o.b;
-    dispatch_slot<RB>(o.a, [&](auto KT) { apply_cx<RB, decltype(KT)::value>(v, kc, c); });
+    op_cx<RB>(o, v, mp.g);
   } else if (o.type == OP_DIAG) {
     for (int k = 0; k < o.nterm; ++k) diag_term<Real, RB, false>(v, mp, terms[o.term + k], mats);
   }
@@ -340,7 +393,6 @@ __device__ __forceinline__ void op_bwd(const KOp& o, Cx<Real>* v, Cx<Real>* l,
     Real m[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) m[i] = mats[o.mat + i];
-    const Real md[8] = {m[0], -m[1], m[4], -m[5], m[2], -m[3], m[6], -m[7]};  // U^dagger
     dispatch_slot<RB>(o.a, [&](auto K) {
       constexpr int k = decltype(K)::value;
       if (o.acc >= 0) {
@@ -348,16 +400,12 @@ __device__ __forceinline__ void op_bwd(const KOp& o, Cx<Real>* v, Cx<Real>* l,
         accum_r<RB, k>(v, l, r);
         warp_sum8(r, lane, width, wacc_w + o.acc);
       }
-      apply_u1<RB, k>(v, md);
-      apply_u1<RB, k>(l, md);
+      apply_u1_dag<RB, k>(v, m);
+      apply_u1_dag<RB, k>(l, m);
     });
   } else if (o.type == OP_CX) {
-    const bool c = (mp.g >> o.cbit) & 1;
-    const int kc = o.b == kExtCtrl ? 0xFF : o.b;
-    dispatch_slot<RB>(o.a, [&](auto KT) {
-      apply_cx<RB, decltype(KT)::value>(v, kc, c);
-      apply_cx<RB, decltype(KT)::value>(l, kc, c);
-    });
+    op_cx<RB>(o, v, mp.g);
+    op_cx<RB>(o, l, mp.g);
   } else if (o.type == OP_DIAG) {
     // gradient: Im(conj(lambda) Z_mask psi) at the op output (all terms commute);
     // Im(conj(l) v) is invariant under the common phase, so order is free.
@@ -379,7 +427,7 @@ __device__ __forceinline__ void op_bwd(const KOp& o, Cx<Real>* v, Cx<Real>* l,
 #pragma unroll
         for (int j = 0; j < (1 << RB); ++j) {
           const uint32_t s = tp ^ (__popc((uint32_t)j & mr) & 1u);
-          const Real tj = l[j].x * v[j].y - l[j].y * v[j].x;
+          const Real tj = fma(l[j].x, v[j].y, -l[j].y * v[j].x);
           acc += s ? -tj : tj;
         }
       }

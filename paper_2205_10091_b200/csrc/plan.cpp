@@ -727,6 +727,12 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
           int cs = loc[o.b1] >= 0 ? slot_of(o.b1) : -1;
           ko.b = cs >= 0 ? (uint8_t)cs : kExtCtrl;
           ko.cbit = (uint8_t)o.b1;
+          if (cs < 0) {  // uniform across a warp unless the control is a lane bit
+            bool lane_bit = false;
+            if (loc[o.b1] >= 0)
+              for (int m = 0; m < std::min(P.h, 5); ++m) lane_bit |= ks.T[m] == loc[o.b1];
+            ko.nterm = lane_bit ? 0 : 1;
+          }
         } else {
           ko.nterm = (int16_t)o.terms.size();
           ko.term = (int)P.kterms.size() - pass.kterm_begin;
