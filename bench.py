@@ -147,6 +147,7 @@ def main():
     ap.add_argument("--batch", type=int, default=None, help="theta rows per rank")
     ap.add_argument("--tile-bits", type=int, default=0)
     ap.add_argument("--max-ops-per-pass", type=int, default=0)
+    ap.add_argument("--jit", type=int, default=1, help="1: per-circuit specialised kernels")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-rows", type=int, default=8)
     ap.add_argument("--cpu-rows", type=int, default=8)
@@ -174,8 +175,12 @@ def main():
     if world > 1 and rank > 0:  # distinct seeded rows per rank (weak scaling)
         theta = W.thetas(B, circ.n_params, 1000 + rank) if args.config != 2 else \
             W.qaoa_thetas(B, 5, 1000 + rank)
-    C = tcx.Circuit(circ, dtype, tile_bits=args.tile_bits, max_ops_per_pass=args.max_ops_per_pass)
+    C = tcx.Circuit(circ, dtype, tile_bits=args.tile_bits, max_ops_per_pass=args.max_ops_per_pass,
+                    jit=bool(args.jit))
     P = tcx.Pauli(H)
+    t_jit = time.perf_counter()
+    C.compile(P, B=B, kind="grad")  # the K.jit analog: excluded from timings
+    t_jit = time.perf_counter() - t_jit
     info = C.info(P)
     th = torch.as_tensor(np.ascontiguousarray(theta)).to(dev)
     E = torch.empty(B, dtype=torch.float64, device=dev)
@@ -296,7 +301,8 @@ def main():
                        2 * B * (2 ** circ.n) * (8 if dtype == "c64" else 16) / 2 ** 30),
                    "plan": {k: info[k] for k in ("tile_bits", "reg_bits", "fwd_passes",
                                                  "lambda_passes", "bwd_passes", "stages",
-                                                 "n_ops")}},
+                                                 "n_ops", "jit")},
+                   "jit_compile_s": round(t_jit, 2)},
         "roofline": roof,
         "kernels": kernel_split,
         "cpu_baseline": cpu,

@@ -92,7 +92,9 @@ typedef struct {
     int32_t reg_bits;       /* r: amplitudes per thread per stage = 2^r (default 4, 3 if n<=t) */
     int32_t coalesce_bits;  /* c: low index bits present in every tile (default: 64 B runs) */
     int32_t max_ops_per_pass; /* fusion depth cap: 0 = light-cone (unlimited), 1 = unfused */
-    int32_t reserved[4];
+    int32_t jit;            /* 0 = per-circuit specialised kernels (NVRTC, sm_100a) when
+                               available, -1 = the precompiled generic kernels */
+    int32_t reserved[3];
 } tcx_build_opts;
 
 /* Executed-plan summary (for reports and tests). */
@@ -106,6 +108,7 @@ typedef struct {
     int32_t stages;           /* register stages summed over forward passes */
     int32_t unitary;          /* 1 if every payload is unitary (grad allowed) */
     int32_t relabeled;        /* 1 if SWAP gates were applied as qubit relabels */
+    int32_t jit;              /* 1 if the passes run per-circuit specialised kernels */
     int64_t tiles_per_state;  /* 2^(n-t) */
     int64_t acc_slots;        /* gradient partial slots per tile */
     int64_t mat_reals;        /* per-theta materialised matrix entries */
@@ -166,6 +169,12 @@ tcx_status tcx_grad_batch_host(const tcx_circuit* circ, const tcx_pauli* pauli,
                                const double* theta_host, int64_t B, double* E_host,
                                double* grad_host, void* ws, size_t ws_bytes,
                                void* cuda_stream);
+
+/* Ahead-of-time specialisation: generate and compile (NVRTC, host only) the per-circuit
+ * kernels a call of `kind` (0 expect, 1 grad, 2 state) needs for B rows; otherwise this
+ * happens on the first compute call.  No-op when the plan runs the generic kernels. */
+tcx_status tcx_circuit_jit(const tcx_circuit* circ, const tcx_pauli* pauli, int64_t B,
+                           int32_t kind);
 
 /* Plan summary. */
 tcx_status tcx_circuit_info(const tcx_circuit* circ, const tcx_pauli* pauli,

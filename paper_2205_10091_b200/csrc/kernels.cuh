@@ -11,435 +11,11 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "device_common.cuh"
 #include "plan.h"
 
 namespace tcx {
 namespace dev {
-
-template <typename Real>
-struct alignas(2 * sizeof(Real)) Cx {
-  Real x, y;
-};
-
-enum {
-  M_INIT = 1, M_LOAD_PSI = 2, M_FWD = 4, M_LAMBDA = 8, M_LOAD_LAM = 16,
-  M_STORE_PSI = 32, M_STORE_LAM = 64, M_BWD = 128
-};
-enum { KM_FWD = 0, KM_BWD = 1, KM_MEGA = 2 };
-
-struct PassArgs {
-  void* psi;
-  void* lam;
-  const void* mats;
-  double* part;
-  double* epart;
-  const KStage* stages;
-  const KOp* ops;
-  const KTerm* terms;
-  const KGroup* groups;
-  const KPTerm* pterms;
-  const uint32_t* swb;     // [16] swizzle images for this dtype
-  uint64_t wmask;
-  int W[16];
-  int n, t, h;
-  int nstages, mat_begin, mat_count, mat_total;
-  int acc_begin, acc_count, acc_total, max_stage_acc;
-  int group_count, e_units, e_index;
-  int mode, tiles_per_cta, last_is_top;
-  int64_t b0;
-};
-
-struct SmemLayout {
-  int xb_psi, xb_lam, mats, wacc, cacc, stages, red, total;
-};
-__host__ __device__ inline int al16(int x) { return (x + 15) & ~15; }
-__host__ __device__ inline SmemLayout smem_layout(int t, int h, int realsz, int mat_count,
-                                                  int max_stage_acc, int acc_count,
-                                                  int nstages, bool two) {
-  SmemLayout L;
-  int off = 0;
-  const int csz = 2 * realsz;
-  L.xb_psi = off;
-  off = al16(off + (csz << t));
-  L.xb_lam = off;
-  if (two) off = al16(off + (csz << t));
-  L.mats = off;
-  off = al16(off + realsz * mat_count);
-  const int nw = ((1 << h) + 31) / 32;
-  L.wacc = off;
-  off = al16(off + realsz * nw * max_stage_acc);
-  L.cacc = off;
-  off = al16(off + 8 * acc_count);
-  L.stages = off;
-  off = al16(off + (int)sizeof(KStage) * nstages);
-  L.red = off;
-  off = al16(off + 8 * 32);
-  L.total = off;
-  return L;
-}
-
-// Thread <-> amplitude mapping of one stage: thread tid holds the amplitudes whose
-// tile-local index has bit T[m] = bit m of tid, bit R[k] = bit k of the slot j.
-template <int RB>
-struct Map {
-  uint32_t sb;        // swizzled smem index of slot 0
-  uint32_t so[RB];    // swizzle image of register bit k
-  uint64_t g;         // global physical index of slot 0
-  uint32_t gp;        // physical bit positions of register bits, 6 bits each
-};
-template <int RB>
-__device__ __forceinline__ int gpos(const Map<RB>& m, int k) {
-  return (m.gp >> (6 * k)) & 63;
-}
-template <int RB>
-__device__ __forceinline__ void make_map(Map<RB>& m, const int8_t* R, const int8_t* T, int h,
-                                         int tid, uint64_t outer, const int8_t* wpos,
-                                         const uint32_t* swb) {
-  m.sb = 0;
-  m.g = outer;
-  for (int i = 0; i < h; ++i)
-    if (tid >> i & 1) {
-      const int l = T[i];
-      m.sb ^= swb[l];
-      m.g |= 1ull << wpos[l];
-    }
-  m.gp = 0;
-#pragma unroll
-  for (int k = 0; k < RB; ++k) {
-    const int l = R[k];
-    m.so[k] = swb[l];
-    m.gp |= (uint32_t)wpos[l] << (6 * k);
-  }
-}
-template <int RB>
-__device__ __forceinline__ void make_top(Map<RB>& m, int h, int tid, uint64_t outer,
-                                         const int8_t* wpos, const uint32_t* swb) {
-  m.sb = 0;
-  m.g = outer;
-  for (int i = 0; i < h; ++i)
-    if (tid >> i & 1) {
-      m.sb ^= swb[i];
-      m.g |= 1ull << wpos[i];
-    }
-  m.gp = 0;
-#pragma unroll
-  for (int k = 0; k < RB; ++k) {
-    m.so[k] = swb[h + k];
-    m.gp |= (uint32_t)wpos[h + k] << (6 * k);
-  }
-}
-template <int RB>
-__device__ __forceinline__ uint32_t sidx(const Map<RB>& m, int j) {
-  uint32_t s = m.sb;
-#pragma unroll
-  for (int k = 0; k < RB; ++k)
-    if (j >> k & 1) s ^= m.so[k];
-  return s;
-}
-template <int RB>
-__device__ __forceinline__ uint64_t gidx(const Map<RB>& m, int j) {
-  uint64_t s = m.g;
-#pragma unroll
-  for (int k = 0; k < RB; ++k)
-    if (j >> k & 1) s |= 1ull << gpos(m, k);
-  return s;
-}
-// register-slot image of a physical mask: bit k set iff register bit k is in mask
-template <int RB>
-__device__ __forceinline__ uint32_t regmask(const Map<RB>& m, uint64_t mask) {
-  uint32_t r = 0;
-#pragma unroll
-  for (int k = 0; k < RB; ++k) r |= (uint32_t)((mask >> gpos(m, k)) & 1ull) << k;
-  return r;
-}
-
-template <int N>
-struct IC {
-  static constexpr int value = N;
-};
-template <int RB, typename F>
-__device__ __forceinline__ void dispatch_slot(int k, F&& f) {
-  switch (k) {
-    case 0: f(IC<0>{}); break;
-    case 1: if constexpr (RB > 1) f(IC<1>{}); break;
-    case 2: if constexpr (RB > 2) f(IC<2>{}); break;
-    case 3: if constexpr (RB > 3) f(IC<3>{}); break;
-    default: break;
-  }
-}
-
-// ---- gate application on register slots -------------------------------------
-// U = [[u00, u01], [u10, u11]] on slot K; m = (u00, u01, u10, u11) as (re, im).
-template <int RB, int K, typename Real>
-__device__ __forceinline__ void apply_u1(Cx<Real>* v, const Real (&m)[8]) {
-#pragma unroll
-  for (int j = 0; j < (1 << RB); ++j) {
-    if (j & (1 << K)) continue;
-    const int j1 = j | (1 << K);
-    const Cx<Real> p = v[j], q = v[j1];
-    v[j].x = m[0] * p.x - m[1] * p.y + m[2] * q.x - m[3] * q.y;
-    v[j].y = m[0] * p.y + m[1] * p.x + m[2] * q.y + m[3] * q.x;
-    v[j1].x = m[4] * p.x - m[5] * p.y + m[6] * q.x - m[7] * q.y;
-    v[j1].y = m[4] * p.y + m[5] * p.x + m[6] * q.y + m[7] * q.x;
-  }
-}
-// U^dagger on slot K from the same m (conj-transpose folded into operand signs).
-template <int RB, int K, typename Real>
-__device__ __forceinline__ void apply_u1_dag(Cx<Real>* v, const Real (&m)[8]) {
-#pragma unroll
-  for (int j = 0; j < (1 << RB); ++j) {
-    if (j & (1 << K)) continue;
-    const int j1 = j | (1 << K);
-    const Cx<Real> p = v[j], q = v[j1];
-    // out0 = conj(u00) p + conj(u10) q ; out1 = conj(u01) p + conj(u11) q
-    v[j].x = m[0] * p.x + m[1] * p.y + m[4] * q.x + m[5] * q.y;
-    v[j].y = m[0] * p.y - m[1] * p.x + m[4] * q.y - m[5] * q.x;
-    v[j1].x = m[2] * p.x + m[3] * p.y + m[6] * q.x + m[7] * q.y;
-    v[j1].y = m[2] * p.y - m[3] * p.x + m[6] * q.y - m[7] * q.x;
-  }
-}
-// R'_ab += psi_a conj(lambda_b) over the pairs of slot K (a, b = value of the bit).
-template <int RB, int K, typename Real>
-__device__ __forceinline__ void accum_r(const Cx<Real>* v, const Cx<Real>* l, Real (&r)[8]) {
-#pragma unroll
-  for (int j = 0; j < (1 << RB); ++j) {
-    if (j & (1 << K)) continue;
-    const int j1 = j | (1 << K);
-    const Cx<Real> p0 = v[j], p1 = v[j1], l0 = l[j], l1 = l[j1];
-    r[0] = fma(p0.x, l0.x, fma(p0.y, l0.y, r[0]));
-    r[1] = fma(p0.y, l0.x, fma(-p0.x, l0.y, r[1]));
-    r[2] = fma(p0.x, l1.x, fma(p0.y, l1.y, r[2]));
-    r[3] = fma(p0.y, l1.x, fma(-p0.x, l1.y, r[3]));
-    r[4] = fma(p1.x, l0.x, fma(p1.y, l0.y, r[4]));
-    r[5] = fma(p1.y, l0.x, fma(-p1.x, l0.y, r[5]));
-    r[6] = fma(p1.x, l1.x, fma(p1.y, l1.y, r[6]));
-    r[7] = fma(p1.y, l1.x, fma(-p1.x, l1.y, r[7]));
-  }
-}
-// CNOT with target slot KT and control register slot KC: register swaps.
-template <int RB, int KT, int KC, typename Real>
-__device__ __forceinline__ void apply_cx_rr(Cx<Real>* v) {
-#pragma unroll
-  for (int j = 0; j < (1 << RB); ++j) {
-    if ((j & (1 << KT)) || !(j & (1 << KC))) continue;
-    const int j1 = j | (1 << KT);
-    const Cx<Real> p = v[j];
-    v[j] = v[j1];
-    v[j1] = p;
-  }
-}
-// CNOT with target slot KT and a control bit outside the registers (thread/tile bit
-// `c`): warp-uniform controls branch, lane-varying ones select.  Self-inverse.
-template <int RB, int KT, typename Real>
-__device__ __forceinline__ void apply_cx_ext(Cx<Real>* v, bool c, bool uniform) {
-  if (uniform) {
-    if (c) {
-#pragma unroll
-      for (int j = 0; j < (1 << RB); ++j) {
-        if (j & (1 << KT)) continue;
-        const Cx<Real> p = v[j];
-        v[j] = v[j | (1 << KT)];
-        v[j | (1 << KT)] = p;
-      }
-    }
-    return;
-  }
-#pragma unroll
-  for (int j = 0; j < (1 << RB); ++j) {
-    if (j & (1 << KT)) continue;
-    const int j1 = j | (1 << KT);
-    const Cx<Real> p = v[j], q = v[j1];
-    v[j].x = c ? q.x : p.x;
-    v[j].y = c ? q.y : p.y;
-    v[j1].x = c ? p.x : q.x;
-    v[j1].y = c ? p.y : q.y;
-  }
-}
-template <int RB, typename Real>
-__device__ __forceinline__ void op_cx(const KOp& o, Cx<Real>* v, uint64_t g) {
-  if (o.b == kExtCtrl) {
-    const bool c = (g >> o.cbit) & 1;
-    const bool uni = o.nterm != 0;  // plan: control is an outer or warp bit
-    dispatch_slot<RB>(o.a, [&](auto KT) { apply_cx_ext<RB, decltype(KT)::value>(v, c, uni); });
-  } else {
-    if constexpr (RB >= 2) {
-      dispatch_slot<RB>(o.a, [&](auto KT) {
-        dispatch_slot<RB>(o.b, [&](auto KC) {
-          if constexpr (decltype(KT)::value != decltype(KC)::value)
-            apply_cx_rr<RB, decltype(KT)::value, decltype(KC)::value>(v);
-        });
-      });
-    }
-  }
-}
-
-// ---- warp reductions -----------------------------------------------------------
-template <typename Real>
-__device__ __forceinline__ Real warp_sum(Real x, int width) {
-  const unsigned mask = width >= 32 ? 0xffffffffu : ((1u << width) - 1u);
-  for (int o = (width >= 32 ? 16 : width >> 1); o > 0; o >>= 1) x += __shfl_xor_sync(mask, x, o);
-  return x;
-}
-// Transposed butterfly: 8 values over 32 lanes in 9 shuffles; lane (l & 3) == 0 ends
-// with value index 4*b4 + 2*b3 + b2 and writes it to dst[index].
-template <typename Real>
-__device__ __forceinline__ void warp_sum8(Real (&r)[8], int lane, int width, Real* dst) {
-  if (width >= 32) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const bool hi = lane & 16;
-      const Real send = hi ? r[k] : r[k + 4];
-      const Real keep = hi ? r[k + 4] : r[k];
-      r[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const bool hi = lane & 8;
-      const Real send = hi ? r[k] : r[k + 2];
-      const Real keep = hi ? r[k + 2] : r[k];
-      r[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
-    {
-      const bool hi = lane & 4;
-      const Real send = hi ? r[0] : r[1];
-      const Real keep = hi ? r[1] : r[0];
-      r[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    }
-    r[0] += __shfl_xor_sync(0xffffffffu, r[0], 2);
-    r[0] += __shfl_xor_sync(0xffffffffu, r[0], 1);
-    if ((lane & 3) == 0) dst[((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1)] = r[0];
-  } else {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) r[k] = warp_sum(r[k], width);
-    if (lane == 0) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) dst[k] = r[k];
-    }
-  }
-}
-
-// ---- shared-memory 4x4 (fixed U2 payload; rare, no register-slot constraint) ----
-template <typename Real, bool DAG>
-__device__ void smem_u2(Cx<Real>* buf, int t, int la, int lb, const Real* m,
-                        const uint32_t* swb, int tid, int nthr) {
-  const int ngroups = 1 << (t - 2);
-  const int lo = la < lb ? la : lb, hi = la < lb ? lb : la;
-  for (int g = tid; g < ngroups; g += nthr) {
-    uint32_t i = g;
-    i = ((i >> lo) << (lo + 1)) | (i & ((1u << lo) - 1));
-    i = ((i >> hi) << (hi + 1)) | (i & ((1u << hi) - 1));
-    uint32_t id[4] = {i, i | (1u << lb), i | (1u << la), i | (1u << la) | (1u << lb)};
-    Cx<Real> in[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      uint32_t s = 0;
-      for (int p = 0; p < t; ++p)
-        if (id[k] >> p & 1) s ^= swb[p];
-      id[k] = s;
-      in[k] = buf[s];
-    }
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      Real ox = 0, oy = 0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const Real mr = DAG ? m[2 * (k * 4 + r)] : m[2 * (r * 4 + k)];
-        const Real mi = DAG ? -m[2 * (k * 4 + r) + 1] : m[2 * (r * 4 + k) + 1];
-        ox += mr * in[k].x - mi * in[k].y;
-        oy += mr * in[k].y + mi * in[k].x;
-      }
-      buf[id[r]] = Cx<Real>{ox, oy};
-    }
-  }
-}
-
-// ---- diagonal phase op: prod_k exp(i w_k (-1)^popc(r & mask_k)) ------------------
-template <typename Real, int RB, bool CONJ>
-__device__ __forceinline__ void diag_term(Cx<Real>* v, const Map<RB>& mp, const KTerm& tm,
-                                          const Real* mats) {
-  const Real cw = mats[tm.wofs], sw = mats[tm.wofs + 1];
-  const uint32_t tp = __popcll(mp.g & tm.mask) & 1u;
-  const uint32_t mr = regmask<RB>(mp, tm.mask);
-#pragma unroll
-  for (int j = 0; j < (1 << RB); ++j) {
-    const uint32_t s = tp ^ (__popc((uint32_t)j & mr) & 1u);
-    const Real ss = (s ^ (CONJ ? 1u : 0u)) ? -sw : sw;
-    const Cx<Real> p = v[j];
-    v[j].x = p.x * cw - p.y * ss;
-    v[j].y = p.x * ss + p.y * cw;
-  }
-}
-
-template <typename Real, int RB>
-__device__ __forceinline__ void op_fwd(const KOp& o, Cx<Real>* v, const Map<RB>& mp,
-                                       const Real* mats, const KTerm* terms) {
-  if (o.type == OP_U1) {
-    Real m[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) m[i] = mats[o.mat + i];
-    dispatch_slot<RB>(o.a, [&](auto K) { apply_u1<RB, decltype(K)::value>(v, m); });
-  } else if (o.type == OP_CX) {
-    op_cx<RB>(o, v, mp.g);
-  } else if (o.type == OP_DIAG) {
-    for (int k = 0; k < o.nterm; ++k) diag_term<Real, RB, false>(v, mp, terms[o.term + k], mats);
-  }
-}
-
-template <typename Real, int RB>
-__device__ __forceinline__ void op_bwd(const KOp& o, Cx<Real>* v, Cx<Real>* l,
-                                       const Map<RB>& mp, const Real* mats, const KTerm* terms,
-                                       Real* wacc_w, int lane, int width) {
-  if (o.type == OP_U1) {
-    Real m[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) m[i] = mats[o.mat + i];
-    dispatch_slot<RB>(o.a, [&](auto K) {
-      constexpr int k = decltype(K)::value;
-      if (o.acc >= 0) {
-        Real r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        accum_r<RB, k>(v, l, r);
-        warp_sum8(r, lane, width, wacc_w + o.acc);
-      }
-      apply_u1_dag<RB, k>(v, m);
-      apply_u1_dag<RB, k>(l, m);
-    });
-  } else if (o.type == OP_CX) {
-    op_cx<RB>(o, v, mp.g);
-    op_cx<RB>(o, l, mp.g);
-  } else if (o.type == OP_DIAG) {
-    // gradient: Im(conj(lambda) Z_mask psi) at the op output (all terms commute);
-    // Im(conj(l) v) is invariant under the common phase, so order is free.
-    int cur = -1;
-    Real acc = 0;
-    for (int k = 0; k < o.nterm; ++k) {
-      const KTerm tm = terms[o.term + k];
-      if (tm.acc >= 0) {
-        if (tm.acc != cur) {
-          if (cur >= 0) {
-            acc = warp_sum(acc, width);
-            if (lane == 0) wacc_w[cur] = acc;
-          }
-          cur = tm.acc;
-          acc = 0;
-        }
-        const uint32_t tp = __popcll(mp.g & tm.mask) & 1u;
-        const uint32_t mr = regmask<RB>(mp, tm.mask);
-#pragma unroll
-        for (int j = 0; j < (1 << RB); ++j) {
-          const uint32_t s = tp ^ (__popc((uint32_t)j & mr) & 1u);
-          const Real tj = fma(l[j].x, v[j].y, -l[j].y * v[j].x);
-          acc += s ? -tj : tj;
-        }
-      }
-      diag_term<Real, RB, true>(v, mp, tm, mats);
-      diag_term<Real, RB, true>(l, mp, tm, mats);
-    }
-    if (cur >= 0) {
-      acc = warp_sum(acc, width);
-      if (lane == 0) wacc_w[cur] = acc;
-    }
-  }
-}
 
 // ---- the window pass kernel --------------------------------------------------
 template <typename Real, int RB, int KM>
@@ -567,43 +143,7 @@ __global__ void __launch_bounds__(256, 2) pass_kernel(const PassArgs a) {
 
     // ------------------------------------------- lambda = H psi, E partial
     if (kFwd && (mode & M_LAMBDA)) {
-      __syncthreads();
-#pragma unroll
-      for (int j = 0; j < NR; ++j) xp[sidx(top, j)] = v[j];
-      __syncthreads();
-      Real e = 0;
-      for (int g = 0; g < a.group_count; ++g) {
-        const KGroup G = a.groups[g];
-        uint32_t swx = 0;
-        for (int p = 0; p < t; ++p)
-          if (G.xlocal >> p & 1u) swx ^= s_swb[p];
-        Real cr[NR], ci[NR];
-#pragma unroll
-        for (int j = 0; j < NR; ++j) cr[j] = ci[j] = 0;
-        for (int k = 0; k < G.term_count; ++k) {
-          const KPTerm pt = a.pterms[G.term_begin + k];
-          const uint32_t tp = __popcll(top.g & pt.zy) & 1u;
-          const uint32_t mr = regmask<RB>(top, pt.zy);
-          const Real re = (Real)pt.cre, im = (Real)pt.cim;
-#pragma unroll
-          for (int j = 0; j < NR; ++j) {
-            const uint32_t s = tp ^ (__popc((uint32_t)j & mr) & 1u);
-            cr[j] += s ? -re : re;
-            ci[j] += s ? -im : im;
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < NR; ++j) {
-          // partner amplitude psi[r ^ x]: from the tile in smem, or (flip mask not
-          // inside the window) gathered from the stored state in global memory
-          const C p = G.global ? gpsi[gidx(top, j) ^ G.xphys] : xp[sidx(top, j) ^ swx];
-          const Real dx = cr[j] * p.x - ci[j] * p.y;
-          const Real dy = cr[j] * p.y + ci[j] * p.x;
-          e += v[j].x * dx + v[j].y * dy;
-          l[j].x += dx;
-          l[j].y += dy;
-        }
-      }
+      const Real e = lambda_tile<Real, RB>(a, v, l, top, xp, gpsi, s_swb, t);
       e_acc += (double)e;
     }
 

@@ -13,13 +13,13 @@
 
 #include "../../include/tcx.h"
 
+#include "device_abi.h"
+
 namespace tcx {
 
-enum : uint8_t { OP_U1 = 1, OP_U2F = 2, OP_CX = 3, OP_DIAG = 4 };
 constexpr int kMaxQubits = 40;
 constexpr int kMaxTileBits = 15;
 constexpr int kMaxRegBits = 4;
-constexpr uint8_t kExtCtrl = 0xFF;
 
 // One original 1-qubit gate folded into a fused U1 op (applied in list order).
 struct Constituent {
@@ -56,37 +56,7 @@ struct Op {
   int acc_off = -1, acc_len = 0; // global partial slots
 };
 
-// ---- kernel tables (POD, copied to the device as-is) ----
-struct KOp {       // 16 bytes
-  uint8_t type, a, b, cbit;  // slots / external control bit
-  int16_t mat;     // offset (Reals) into the pass's smem matrix table
-  int16_t nterm;   // DIAG terms
-  int32_t acc;     // stage-local acc slot base, -1 none
-  int32_t term;    // DIAG: first KTerm (pass-relative)
-};
-struct KTerm {     // 16 bytes
-  uint64_t mask;   // physical bits
-  int16_t wofs;    // (cos, sin) pair offset in the pass matrix table
-  int16_t acc;     // stage-local acc slot, -1 none
-  int32_t pad;
-};
-struct KStage {    // 48 bytes
-  int8_t R[8];     // local positions of register slots k < r
-  int8_t T[16];    // local positions of thread bits m < h (lanes first)
-  int32_t op_begin, op_count;      // pass-relative KOp range
-  int32_t acc_begin, acc_count;    // pass-relative slot range
-  int32_t same_as_prev, pad;       // 1: identical mapping to the previous stage
-};
-struct KGroup {    // Pauli terms sharing one X/Y flip mask
-  uint64_t xphys;     // flip mask, physical bits
-  uint32_t xlocal;    // flip mask in tile-local bits (global == 0)
-  int32_t term_begin, term_count;
-  int32_t global;     // 1: partner amplitudes gathered from global memory
-};
-struct KPTerm {    // 24 bytes: coefficient alpha_j * i^nY * (-1)^popc(x & zy)
-  uint64_t zy;     // physical Y|Z mask
-  double cre, cim;
-};
+
 // materialize items (per theta): U1 product, U2F copy, diag (cos, sin)
 struct MItem {
   int32_t type;      // OP_U1 / OP_U2F / OP_DIAG(term)
@@ -149,6 +119,12 @@ struct Binding {        // (circuit, pauli) specific lambda schedule
 
 struct DeviceTables;
 
+struct JitKernel {      // NVRTC-compiled specialisation of one pass (jit.cpp)
+  int pass = 0, km = 0; // km: 0 forward, 1 backward, 2 fused single pass
+  std::string name;
+  std::vector<char> cubin;
+};
+
 struct Plan {
   int n = 0, P = 0;
   tcx_dtype dtype = TCX_C64;
@@ -173,6 +149,11 @@ struct Plan {
   bool relabeled = false;
   bool unitary = true;
   int64_t tiles = 1;             // 2^(n - t)
+
+  bool jit_on = false;             // per-circuit specialised kernels (compiled lazily)
+  std::map<int, JitKernel> jit;    // key pass*4 + km -> compiled CUBIN
+  std::string jit_note;            // why JIT is off, if it is
+  std::mutex jit_mu;
 
   std::mutex mu;
   std::map<const void*, std::shared_ptr<Binding>> bindings;

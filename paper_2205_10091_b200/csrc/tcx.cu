@@ -7,6 +7,7 @@
 //                       adjoint backward stages with <lambda|dG|psi> partials (a7)
 //   finalize_kernel     deterministic fp64 reductions -> E[B], grad[B][P] (a8)
 // Every step of the path runs in these kernels; there is no host fallback.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -17,6 +18,7 @@
 #include <string>
 #include <type_traits>
 
+#include "jit.h"
 #include "kernels.cuh"
 #include "plan.h"
 
@@ -248,6 +250,8 @@ struct DevBuf {
 namespace tcx {
 struct DeviceTables {
   DevBuf kops, kterms, kstages, mitems, dcons, gitems, pptr, plist, fixed, layout, swb;
+  std::map<int, CUfunction> jit;    // key pass*4 + km
+  std::map<int, size_t> jit_smem;   // dynamic smem opted in per function
 };
 }  // namespace tcx
 
@@ -266,6 +270,32 @@ tcx_status upload(DevBuf& d, const std::vector<T>& v) {
   CUDA_TRY(cudaMalloc(&d.p, bytes));
   if (!v.empty()) CUDA_TRY(cudaMemcpy(d.p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
   return TCX_OK;
+}
+
+// Driver API through the runtime's entry-point query (no link-time libcuda dependency).
+struct Drv {
+  bool ok = false;
+  CUresult (*moduleLoadData)(CUmodule*, const void*);
+  CUresult (*moduleGetFunction)(CUfunction*, CUmodule, const char*);
+  CUresult (*launchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                           unsigned, CUstream, void**, void**);
+  CUresult (*funcSetAttribute)(CUfunction, CUfunction_attribute, int);
+};
+Drv& drv() {
+  static Drv D;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    auto get = [](const char* name, void** fp) {
+      cudaDriverEntryPointQueryResult q;
+      return cudaGetDriverEntryPoint(name, fp, cudaEnableDefault, &q) == cudaSuccess &&
+             q == cudaDriverEntryPointSuccess;
+    };
+    D.ok = get("cuModuleLoadData", (void**)&D.moduleLoadData) &&
+           get("cuModuleGetFunction", (void**)&D.moduleGetFunction) &&
+           get("cuLaunchKernel", (void**)&D.launchKernel) &&
+           get("cuFuncSetAttribute", (void**)&D.funcSetAttribute);
+  });
+  return D;
 }
 
 tcx_status device_tables(Plan& P, DeviceTables*& out) {
@@ -292,6 +322,56 @@ tcx_status device_tables(Plan& P, DeviceTables*& out) {
   if ((s = upload(T->layout, lay))) return s;
   out = T.get();
   P.dev[dev] = T;
+  return TCX_OK;
+}
+
+// Specialised kernel for (pass, km): compiled (NVRTC / disk cache) and loaded into this
+// device's context on first use.  Returns nullptr when the plan runs generic kernels.
+tcx_status jit_function(Plan& P, DeviceTables* DT, int key, CUfunction* f) {
+  *f = nullptr;
+  if (!P.jit_on) return TCX_OK;
+  {
+    std::lock_guard<std::mutex> lk(P.mu);
+    auto it = DT->jit.find(key);
+    if (it != DT->jit.end()) {
+      *f = it->second;
+      return TCX_OK;
+    }
+  }
+  std::string err;
+  if (!jit_build(P, {key}, err)) return fail(TCX_E_CUDA, err);
+  Drv& D = drv();
+  if (!D.ok) return fail(TCX_E_CUDA, "driver entry points unavailable for JIT kernels");
+  CUDA_TRY(cudaFree(0));  // primary context current on this thread
+  CUmodule m;
+  CUfunction fn;
+  const JitKernel& k = P.jit.at(key);
+  if (D.moduleLoadData(&m, k.cubin.data()) != CUDA_SUCCESS)
+    return fail(TCX_E_CUDA, "cuModuleLoadData failed for " + k.name);
+  if (D.moduleGetFunction(&fn, m, k.name.c_str()) != CUDA_SUCCESS)
+    return fail(TCX_E_CUDA, "cuModuleGetFunction failed for " + k.name);
+  std::lock_guard<std::mutex> lk(P.mu);
+  DT->jit[key] = fn;
+  DT->jit_smem[key] = 0;
+  *f = fn;
+  return TCX_OK;
+}
+
+// Compile every specialised kernel a call of this kind needs, in parallel, before launching.
+tcx_status jit_prepare(Plan& P, int kind, bool mega) {
+  if (!P.jit_on) return TCX_OK;
+  std::vector<int> keys;
+  const int nP = (int)P.passes.size();
+  if (mega) {
+    keys.push_back(kind == 1 ? 2 : 0);
+  } else {
+    for (int p = 0; p < nP; ++p) {
+      keys.push_back(p * 4 + 0);
+      if (kind == 1) keys.push_back(p * 4 + 1);
+    }
+  }
+  std::string err;
+  if (!jit_build(P, keys, err)) return fail(TCX_E_CUDA, err);
   return TCX_OK;
 }
 
@@ -438,6 +518,7 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
   if (ws_bytes < wl.total)
     return fail(TCX_E_INVALID, "workspace too small: need " + std::to_string(wl.total) +
                                    " bytes, got " + std::to_string(ws_bytes));
+  if ((s = jit_prepare(P, kind, wl.mega))) return s;
   char* W = (char*)ws;
   const bool c128 = P.dtype == TCX_C128;
   const int rs = c128 ? 8 : 4;
@@ -502,7 +583,7 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
     a.max_stage_acc = p.max_stage_acc;
     a.last_is_top = p.last_is_top;
   };
-  auto launch_raw = [&](PassArgs& a) -> tcx_status {
+  auto launch_raw = [&](PassArgs& a, int jit_pass) -> tcx_status {
     const bool fwd = (a.mode & (M_FWD | M_LAMBDA)) != 0;
     const bool two = (a.mode & M_BWD) != 0;
     const int km = (fwd && two) ? KM_MEGA : (two ? KM_BWD : KM_FWD);
@@ -516,9 +597,29 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
     if (L.total > 227 * 1024 - 256)
       return fail(TCX_E_UNSUPPORTED, "pass needs " + std::to_string(L.total) +
                                          " B of shared memory (> 227 KB); lower tile_bits");
+    CUfunction jf = nullptr;  // specialised kernel for this pass and mode
+    const int jkey = jit_pass * 4 + km;
+    if (jit_pass >= 0) {
+      tcx_status js = jit_function(P, DT, jkey, &jf);
+      if (js) return js;
+    }
     for (int64_t b0 = 0; b0 < B; b0 += kMaxRows) {
       const int64_t rows = std::min(kMaxRows, B - b0);
       a.b0 = b0;
+      if (jf) {
+        Drv& D = drv();
+        if (L.total > 48 * 1024 && (size_t)L.total > DT->jit_smem[jkey]) {
+          if (D.funcSetAttribute(jf, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, L.total) !=
+              CUDA_SUCCESS)
+            return fail(TCX_E_CUDA, "cuFuncSetAttribute failed for " + jit_kernel_name(jit_pass, km));
+          DT->jit_smem[jkey] = L.total;
+        }
+        void* params[] = {&a};
+        if (D.launchKernel(jf, (unsigned)S, (unsigned)rows, 1, 1u << a.h, 1, 1, (unsigned)L.total,
+                           (CUstream)st, params, nullptr) != CUDA_SUCCESS)
+          return fail(TCX_E_CUDA, "cuLaunchKernel failed for " + jit_kernel_name(jit_pass, km));
+        continue;
+      }
       cudaError_t e;
       if (c128)
         e = km == 0 ? launch_f64_0(P.r, a, S, rows, L.total, st)
@@ -534,13 +635,14 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
   };
   const double Nf = (double)((int64_t)1 << P.n), csz = 2.0 * rs, Bf = (double)B;
   auto launch = [&](PassArgs& a, int phase, int index, double flops_amp) -> tcx_status {
+    const int jit_pass = (phase == 1 || phase == 3 || phase == 5) ? index : -1;
     ProfEntry pe{};
     if (g_prof.on) {
       CUDA_TRY(cudaEventCreate(&pe.a));
       CUDA_TRY(cudaEventCreate(&pe.b));
       CUDA_TRY(cudaEventRecord(pe.a, st));
     }
-    tcx_status r0 = launch_raw(a);
+    tcx_status r0 = launch_raw(a, jit_pass);
     if (r0) return r0;
     if (g_prof.on) {
       CUDA_TRY(cudaEventRecord(pe.b, st));
@@ -686,6 +788,19 @@ tcx_status tcx_circuit_build(int32_t n_qubits, int32_t n_params, const tcx_gate*
     delete c;
     return fail(s, err);
   }
+  if (!opts || opts->jit >= 0) {
+    std::string why;
+    const Plan& P = c->plan;
+    if (!jit_available(&why)) {
+      c->plan.jit_note = why;
+    } else if (P.passes.size() > 48 || P.ops.size() > 4096) {
+      c->plan.jit_note = "circuit too large for per-pass specialisation";
+    } else {
+      c->plan.jit_on = true;  // kernels are generated and compiled on first use
+    }
+  } else {
+    c->plan.jit_note = "disabled by tcx_build_opts.jit";
+  }
   *out = c;
   return TCX_OK;
 }
@@ -798,6 +913,21 @@ tcx_status tcx_grad_batch_host(const tcx_circuit* circ, const tcx_pauli* pauli,
   return host_call(circ, pauli, theta_host, B, E_host, grad_host, ws, ws_bytes, stream, K_GRAD);
 }
 
+tcx_status tcx_circuit_jit(const tcx_circuit* circ, const tcx_pauli* pauli, int64_t B,
+                           int32_t kind) {
+  g_err.clear();
+  if (!circ || B <= 0 || kind < 0 || kind > 2) return fail(TCX_E_INVALID, "bad argument");
+  Plan& P = const_cast<tcx_circuit*>(circ)->plan;
+  std::shared_ptr<Binding> Bd;
+  if (kind != K_STATE) {
+    if (!pauli) return fail(TCX_E_INVALID, "null pauli");
+    tcx_status s = binding_for(P, pauli, Bd, nullptr);
+    if (s) return s;
+  }
+  WsLayout wl = ws_layout(P, Bd.get(), B, kind, false);
+  return jit_prepare(P, kind, wl.mega);
+}
+
 tcx_status tcx_circuit_info(const tcx_circuit* circ, const tcx_pauli* pauli, tcx_plan_info* o) {
   g_err.clear();
   if (!circ || !o) return fail(TCX_E_INVALID, "null argument");
@@ -818,6 +948,7 @@ tcx_status tcx_circuit_info(const tcx_circuit* circ, const tcx_pauli* pauli, tcx
   o->stages = st;
   o->unitary = P.unitary;
   o->relabeled = P.relabeled;
+  o->jit = P.jit_on ? 1 : 0;
   o->tiles_per_state = P.tiles;
   o->acc_slots = P.acc_total;
   o->mat_reals = P.mat_total;

@@ -44,14 +44,14 @@ class tcx_gate(ctypes.Structure):
 class tcx_build_opts(ctypes.Structure):
     _fields_ = [("tile_bits", ctypes.c_int32), ("reg_bits", ctypes.c_int32),
                 ("coalesce_bits", ctypes.c_int32), ("max_ops_per_pass", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 4)]
+                ("jit", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
 
 
 class tcx_plan_info(ctypes.Structure):
     _fields_ = [(f, ctypes.c_int32) for f in (
         "n_qubits", "n_params", "dtype", "tile_bits", "reg_bits", "coalesce_bits",
         "threads_per_tile", "n_ops", "fwd_passes", "lambda_passes", "bwd_passes", "stages",
-        "unitary", "relabeled")] + [(f, ctypes.c_int64) for f in (
+        "unitary", "relabeled", "jit")] + [(f, ctypes.c_int64) for f in (
             "tiles_per_state", "acc_slots", "mat_reals")]
 
     def as_dict(self):
@@ -82,6 +82,7 @@ _sig = {
     "tcx_circuit_layout": [_vp, ctypes.POINTER(_i32)],
     "tcx_launch_count": [_vp, _vp, _i64, _i32, ctypes.POINTER(_i32)],
     "tcx_profile_enable": [_i32],
+    "tcx_circuit_jit": [_vp, _vp, _i64, _i32],
     "tcx_profile_read": [ctypes.POINTER(tcx_kernel_time), _i32, ctypes.POINTER(_i32)],
 }
 for _name, _args in _sig.items():
@@ -128,7 +129,8 @@ class Circuit:
     """tcx_circuit_build over a gate list (workloads.Circuit or raw arrays)."""
 
     def __init__(self, circ, dtype: str = "c64", tile_bits: int = 0, reg_bits: int = 0,
-                 coalesce_bits: int = 0, max_ops_per_pass: int = 0, gates=None):
+                 coalesce_bits: int = 0, max_ops_per_pass: int = 0, jit: bool = True,
+                 gates=None):
         names, q0, q1, param, coeff, moff, mats = circ.arrays()
         self.n = circ.n
         self.P = circ.n_params
@@ -139,7 +141,8 @@ class Circuit:
         if mats.size == 0:
             mats = np.zeros(2)
         self._mats = mats
-        opts = tcx_build_opts(tile_bits, reg_bits, coalesce_bits, max_ops_per_pass)
+        opts = tcx_build_opts(tile_bits, reg_bits, coalesce_bits, max_ops_per_pass,
+                              0 if jit else -1)
         h = _vp()
         _check(_lib.tcx_circuit_build(self.n, self.P, self._gates, self.G,
                                       mats.ctypes.data_as(_dp), mats.size // 2,
@@ -156,6 +159,11 @@ class Circuit:
         out = tcx_plan_info()
         _check(_lib.tcx_circuit_info(self.h, pauli.h if pauli else None, ctypes.byref(out)))
         return out.as_dict()
+
+    def compile(self, pauli=None, B: int = 1, kind: str = "grad"):
+        """Ahead-of-time JIT of the per-circuit kernels (host only; see tcx_circuit_jit)."""
+        k = {"expect": 0, "grad": 1, "state": 2}[kind]
+        _check(_lib.tcx_circuit_jit(self.h, pauli.h if pauli else None, B, k))
 
     def decode(self):
         n = _i64()

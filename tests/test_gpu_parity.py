@@ -42,12 +42,13 @@ def oracle_grad(c, H, theta):
 
 
 # ------------------------------------------------------------------- states
+@pytest.mark.parametrize("jit", [True, False])
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
 @pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 11])
-def test_state_random_all_kinds_single_tile(tc, dtype, n):
+def test_state_random_all_kinds_single_tile(tc, dtype, n, jit):
     c = W.random_circuit(n, 60, 1000 + n, n_params=5)
     th = W.thetas(3, 5, n)
-    C = tc.Circuit(c, dtype)
+    C = tc.Circuit(c, dtype, jit=jit)
     psi = tc.state_batch(C, _th(th)).cpu().numpy()
     for b in range(3):
         ref = orc.state(c, th[b])
@@ -55,13 +56,14 @@ def test_state_random_all_kinds_single_tile(tc, dtype, n):
         assert err <= state_tol(dtype, len(c.gates)), f"row {b}: {err}"
 
 
+@pytest.mark.parametrize("jit", [True, False])
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
 @pytest.mark.parametrize("n,t", [(10, 5), (13, 7), (14, 9), (15, 8)])
-def test_state_multi_pass(tc, dtype, n, t):
+def test_state_multi_pass(tc, dtype, n, t, jit):
     """Several windows and tiles per state (small tile_bits forces many passes)."""
     c = W.random_circuit(n, 120, 2000 + n, n_params=6)
     th = W.thetas(2, 6, n)
-    C = tc.Circuit(c, dtype, tile_bits=t, coalesce_bits=2)
+    C = tc.Circuit(c, dtype, tile_bits=t, coalesce_bits=2, jit=jit)
     info = C.info()
     assert info["tiles_per_state"] > 1 and info["fwd_passes"] > 1
     psi = tc.state_batch(C, _th(th)).cpu().numpy()
@@ -90,27 +92,29 @@ def test_batched_vqe_golden_on_gpu(tc):
 
 
 # -------------------------------------------------------------- E + gradient
+@pytest.mark.parametrize("jit", [True, False])
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
 @pytest.mark.parametrize("seed", range(4))
-def test_grad_random_circuits(tc, dtype, seed):
+def test_grad_random_circuits(tc, dtype, seed, jit):
     n = 3 + seed * 2
     c = W.random_circuit(n, 80, 3000 + seed, n_params=7, with_payload=True)
     H = W.random_pauli_sum(n, 10, seed)
     th = W.thetas(5, 7, seed)
-    E, G, _ = run_grad(tc, c, H, th, dtype)
+    E, G, _ = run_grad(tc, c, H, th, dtype, jit=jit)
     Er, Gr = oracle_grad(c, H, th)
     check_E(E, Er, H, dtype, "E")
     check_grad(G, Gr, H, c, dtype, "grad")
 
 
+@pytest.mark.parametrize("jit", [True, False])
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
 @pytest.mark.parametrize("n,t,seed", [(12, 7, 0), (14, 8, 1), (13, 6, 2)])
-def test_grad_multi_pass_random(tc, dtype, n, t, seed):
+def test_grad_multi_pass_random(tc, dtype, n, t, seed, jit):
     """Multi-pass forward, extra lambda passes, multi-pass backward, several tiles."""
     c = W.random_circuit(n, 90, 4000 + seed, n_params=6)
     H = W.random_pauli_sum(n, 12, 40 + seed)
     th = W.thetas(3, 6, seed)
-    E, G, C = run_grad(tc, c, H, th, dtype, tile_bits=t, coalesce_bits=2)
+    E, G, C = run_grad(tc, c, H, th, dtype, tile_bits=t, coalesce_bits=2, jit=jit)
     info = C.info(tc.Pauli(H))
     assert info["fwd_passes"] > 1
     Er, Gr = oracle_grad(c, H, th)
@@ -118,12 +122,14 @@ def test_grad_multi_pass_random(tc, dtype, n, t, seed):
     check_grad(G, Gr, H, c, dtype, "grad")
 
 
+@pytest.mark.parametrize("jit", [True, False])
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
-def test_grad_hea_heisenberg_multi_tile(tc, dtype):
+def test_grad_hea_heisenberg_multi_tile(tc, dtype, jit):
     n, d = 14, 4
     c, H = W.hea(n, d), W.heisenberg(n)
     th = W.thetas(4, c.n_params, 7)
-    E, G, C = run_grad(tc, c, H, th, dtype, tile_bits=10)
+    E, G, C = run_grad(tc, c, H, th, dtype, tile_bits=10, jit=jit)
+    assert C.info()["jit"] == int(jit)
     info = C.info(tc.Pauli(H))
     assert info["fwd_passes"] > 1 and info["lambda_passes"] >= 1
     Er, Gr = oracle_grad(c, H, th)
@@ -152,13 +158,14 @@ def test_cfg1_full_vs_oracle(tc):
     check_grad(G, Gr, H, c, dt)
 
 
-def test_qaoa_small_vs_oracle(tc):
+@pytest.mark.parametrize("jit", [True, False])
+def test_qaoa_small_vs_oracle(tc, jit):
     n = 12
     edges = W.random_regular_graph(n, 3, 3)
     c, H = W.qaoa_maxcut(n, 3, edges), W.maxcut_cost(n, edges)
     th = W.qaoa_thetas(8, 3, 3)
     for dtype in ("c64", "c128"):
-        E, G, _ = run_grad(tc, c, H, th, dtype, tile_bits=8)
+        E, G, _ = run_grad(tc, c, H, th, dtype, tile_bits=8, jit=jit)
         Er, Gr = oracle_grad(c, H, th)
         check_E(E, Er, H, dtype)
         check_grad(G, Gr, H, c, dtype)
