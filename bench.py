@@ -258,8 +258,14 @@ def main():
     roof = None
     if dom:
         kms, fl, byt, cnt = by[dom]
-        lanes = 64 if dtype == "c128" else 128
-        alu_peak = 148 * lanes * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6  # flop/s
+        try:  # measured FMA throughput (tools/ubench_fma.cu), else unit counts x clock
+            alu = json.load(open(os.path.join(ROOT, "profiles", "alu_peaks.json")))
+            alu_peak = 1e12 * alu["fp64_tflops" if dtype == "c128" else "fp32_tflops"]
+            alu_src = "measured (profiles/alu_peaks.json)"
+        except Exception:
+            lanes = 64 if dtype == "c128" else 128
+            alu_peak = 148 * lanes * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6  # flop/s
+            alu_src = "derived: 148 SMs x lanes x 2 x sm_max_mhz"
         hbm_peak = peaks.get("hbm_gbs", 6650.0) * 1e9
         t_alu, t_hbm = fl / alu_peak, byt / hbm_peak
         if t_alu >= t_hbm:
@@ -271,7 +277,8 @@ def main():
             roof = {"bound": "hbm", "achieved": ach, "peak": hbm_peak / 1e9, "unit": "GB/s",
                     "frac": ach / (hbm_peak / 1e9)}
         roof.update({"kernel": f"pass_kernel ({dom} passes)", "launches": cnt,
-                     "share_of_step": kms / total_k, "peak_source": peak_src,
+                     "share_of_step": kms / total_k,
+                     "peak_source": alu_src if roof["bound"] == "alu" else peak_src + " (MEASURED_PEAKS.json hbm_gbs)",
                      "hbm_achieved_gbs": byt / (kms / 1e3) / 1e9,
                      "traffic": load_traffic(args.config, dom, cnt, args.steps)})
     kernel_split = {k: {"ms": v[0] / args.steps, "launches_per_step": v[3] / args.steps,

@@ -92,18 +92,19 @@ struct SmemLayout {
 };
 TCX_HD inline int al16(int x) { return (x + 15) & ~15; }
 TCX_HD inline SmemLayout smem_layout(int t, int h, int realsz, int mat_count,
-                                                  int max_stage_acc, int acc_count,
-                                                  int nstages, bool two) {
+                                     int max_stage_acc, int acc_count, int nstages, bool two,
+                                     int nsub = 1) {
+  // nsub lock-stepped sub-tiles per CTA (JIT kernels): one exchange buffer each
   SmemLayout L;
   int off = 0;
   const int csz = 2 * realsz;
   L.xb_psi = off;
-  off = al16(off + (csz << t));
+  off = al16(off + nsub * (csz << t));
   L.xb_lam = off;
-  if (two) off = al16(off + (csz << t));
+  if (two) off = al16(off + nsub * (csz << t));
   L.mats = off;
   off = al16(off + realsz * mat_count);
-  const int nw = ((1 << h) + 31) / 32;
+  const int nw = nsub * (((1 << h) + 31) / 32);
   L.wacc = off;
   off = al16(off + realsz * nw * max_stage_acc);
   L.cacc = off;

@@ -87,6 +87,60 @@ __device__ __forceinline__ uint32_t regmask(const Map<RB>& m, uint64_t mask) {
   return r;
 }
 
+// ---- packed FP32x2 arithmetic (sm_100a FFMA2/FMUL2): a complex64 amplitude (x, y) is one
+// 64-bit register pair; broadcast / half-swapped / sign-alternated operands are free
+// operand modifiers in SASS, so a complex multiply-add is 2 instructions instead of 4.
+__device__ __forceinline__ unsigned long long f2u_(Cx<float> v) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(v.x), "f"(v.y));
+  return r;
+}
+__device__ __forceinline__ Cx<float> u2f_(unsigned long long r) {
+  Cx<float> v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+__device__ __forceinline__ Cx<float> f2fma(Cx<float> a, Cx<float> b, Cx<float> c) {  // a*b+c
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2u_(a)), "l"(f2u_(b)), "l"(f2u_(c)));
+  return u2f_(d);
+}
+__device__ __forceinline__ Cx<float> f2mul(Cx<float> a, Cx<float> b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u_(a)), "l"(f2u_(b)));
+  return u2f_(d);
+}
+
+// 64-bit packed complex64 (x in the low half, y in the high half): the operand form of
+// FFMA2 / FMUL2.  Keeping amplitudes in aligned 64-bit registers avoids pair moves.
+typedef unsigned long long q64;
+__device__ __forceinline__ q64 qpk(float a, float b) {
+  q64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float qx(q64 v) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  return a;
+}
+__device__ __forceinline__ float qy(q64 v) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  return b;
+}
+__device__ __forceinline__ q64 qsw(q64 v) { return qpk(qy(v), qx(v)); }
+__device__ __forceinline__ q64 qfma(q64 a, q64 b, q64 c) {  // a * b + c, per half
+  q64 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ q64 qmul(q64 a, q64 b) {
+  q64 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
 template <int N>
 struct IC {
   static constexpr int value = N;
@@ -310,7 +364,7 @@ __device__ __forceinline__ void op_fwd(const KOp& o, Cx<Real>* v, const Map<RB>&
   if (o.type == OP_U1) {
     Real m[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) m[i] = mats[o.mat + i];
+    for (int i = 0; i < 8; ++i) m[i] = mats[o.mat + (sizeof(Real) == 4 ? 2 * i + 1 : i)];
     dispatch_slot<RB>(o.a, [&](auto K) { apply_u1<RB, decltype(K)::value>(v, m); });
   } else if (o.type == OP_CX) {
     op_cx<RB>(o, v, mp.g);
@@ -326,7 +380,7 @@ __device__ __forceinline__ void op_bwd(const KOp& o, Cx<Real>* v, Cx<Real>* l,
   if (o.type == OP_U1) {
     Real m[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) m[i] = mats[o.mat + i];
+    for (int i = 0; i < 8; ++i) m[i] = mats[o.mat + (sizeof(Real) == 4 ? 2 * i + 1 : i)];
     dispatch_slot<RB>(o.a, [&](auto K) {
       constexpr int k = decltype(K)::value;
       if (o.acc >= 0) {

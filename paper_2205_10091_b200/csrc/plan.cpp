@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 #include <complex>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <set>
@@ -176,9 +177,13 @@ double op_weight(const Op& o) {
     default: return 2.0 + 4.0 * (double)o.terms.size();
   }
 }
+// Per-theta table entries (Reals).  complex64 U1 ops store the 2x2 as 16 packed FP32x2
+// coefficient pairs (forward and adjoint forms) so the FFMA2 operands
+// load straight into aligned register pairs; complex128 stores the plain 8 Reals.
+thread_local bool g_packed_u1 = false;
 int op_mats(const Op& o) {
   switch (o.type) {
-    case OP_U1: return 8;
+    case OP_U1: return g_packed_u1 ? 32 : 8;
     case OP_U2F: return 32;
     case OP_CX: return 0;
     default: return 2 * (int)o.terms.size();
@@ -540,6 +545,11 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
   P.h = t - r;
   P.max_ops_per_pass = opts ? std::max(0, opts->max_ops_per_pass) : 0;
   P.tiles = 1ll << (n - t);
+  P.tpc = (int)std::min<int64_t>(64, std::max<int64_t>(1, P.tiles / 32));
+  // two lock-stepped sub-tiles (512 threads) share one instruction stream in the JIT
+  // kernels when tiles pair up and a sub-tile has whole warps
+  P.jit_nsub = (P.tpc % 2 == 0 && P.h >= 5) ? 2 : 1;
+  if (const char* e = getenv("TCX_JIT_NSUB")) P.jit_nsub = std::max(1, std::min(P.jit_nsub, atoi(e)));
   // ---- lower
   int pos[kMaxQubits];
   for (int q = 0; q < n; ++q) pos[q] = n - 1 - q;  // PAPER.md:249 qubit 0 = MSB
@@ -631,6 +641,7 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
   for (int q = 0; q < n; ++q) P.layout[q] = pos[q];
 
   // ---- pass scheduling
+  g_packed_u1 = dtype == TCX_C64;
   Scheduler S(P);
   const int rb = c128 ? 8 : 4;  // bytes per Real
   S.pass_budget.mats = (24 * 1024) / rb;

@@ -149,6 +149,8 @@ struct Plan {
   bool relabeled = false;
   bool unitary = true;
   int64_t tiles = 1;             // 2^(n - t)
+  int tpc = 1;                   // tiles per CTA (depends on the tile count only, never on B)
+  int jit_nsub = 1;              // lock-stepped sub-tiles per CTA in JIT kernels
 
   bool jit_on = false;             // per-circuit specialised kernels (compiled lazily)
   std::map<int, JitKernel> jit;    // key pass*4 + km -> compiled CUBIN

@@ -117,9 +117,24 @@ __global__ void materialize_kernel(const MatArgs a) {
       gate1(a.cons[it.cons_begin + c], th, a.fixed, G);
       mat2mul(G, M, M);
     }
-    for (int k = 0; k < 4; ++k) {
-      out[it.mat_off + 2 * k] = (Real)M[k].x;
-      out[it.mat_off + 2 * k + 1] = (Real)M[k].y;
+    if (sizeof(Real) == 8) {
+      for (int k = 0; k < 4; ++k) {
+        out[it.mat_off + 2 * k] = (Real)M[k].x;
+        out[it.mat_off + 2 * k + 1] = (Real)M[k].y;
+      }
+    } else {
+      // packed complex64 layout: m_i = (re, im) of u00, u01, u10, u11 flattened to m0..m7;
+      // forward pairs (m_i, m_i) / (-m_i, m_i) for even / odd i, then the adjoint pairs
+      // (m0,m0) (m1,-m1) (m4,m4) (m5,-m5) (m2,m2) (m3,-m3) (m6,m6) (m7,-m7).
+      const double m[8] = {M[0].x, M[0].y, M[1].x, M[1].y, M[2].x, M[2].y, M[3].x, M[3].y};
+      static const int dsrc[8] = {0, 1, 4, 5, 2, 3, 6, 7};
+      for (int i = 0; i < 8; ++i) {
+        out[it.mat_off + 2 * i] = (Real)((i & 1) ? -m[i] : m[i]);
+        out[it.mat_off + 2 * i + 1] = (Real)m[i];
+        const double d = m[dsrc[i]];
+        out[it.mat_off + 16 + 2 * i] = (Real)d;
+        out[it.mat_off + 16 + 2 * i + 1] = (Real)((i & 1) ? -d : d);
+      }
     }
   } else if (it.type == OP_U2F) {
     for (int k = 0; k < 32; ++k) out[it.mat_off + k] = (Real)a.fixed[2 * it.payload + k];
@@ -419,11 +434,7 @@ tcx_status binding_for(Plan& P, const tcx_pauli* H, std::shared_ptr<Binding>& ou
   return TCX_OK;
 }
 
-int tiles_per_cta(const Plan& P) {
-  int64_t T = P.tiles;
-  int64_t tpc = std::min<int64_t>(64, std::max<int64_t>(1, T / 32));
-  return (int)tpc;
-}
+int tiles_per_cta(const Plan& P) { return P.tpc; }
 
 enum { K_EXPECT = 0, K_GRAD = 1, K_STATE = 2 };
 
@@ -608,15 +619,20 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
       a.b0 = b0;
       if (jf) {
         Drv& D = drv();
-        if (L.total > 48 * 1024 && (size_t)L.total > DT->jit_smem[jkey]) {
-          if (D.funcSetAttribute(jf, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, L.total) !=
+        const int ns = P.jit_nsub;
+        const SmemLayout LJ = smem_layout(a.t, a.h, rs, a.mat_count, a.max_stage_acc,
+                                          (a.mode & M_BWD) ? a.acc_count : 0, a.nstages, two, ns);
+        if (LJ.total > 227 * 1024 - 256)
+          return fail(TCX_E_UNSUPPORTED, "JIT pass needs too much shared memory");
+        if (LJ.total > 48 * 1024 && (size_t)LJ.total > DT->jit_smem[jkey]) {
+          if (D.funcSetAttribute(jf, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, LJ.total) !=
               CUDA_SUCCESS)
             return fail(TCX_E_CUDA, "cuFuncSetAttribute failed for " + jit_kernel_name(jit_pass, km));
-          DT->jit_smem[jkey] = L.total;
+          DT->jit_smem[jkey] = LJ.total;
         }
         void* params[] = {&a};
-        if (D.launchKernel(jf, (unsigned)S, (unsigned)rows, 1, 1u << a.h, 1, 1, (unsigned)L.total,
-                           (CUstream)st, params, nullptr) != CUDA_SUCCESS)
+        if (D.launchKernel(jf, (unsigned)S, (unsigned)rows, 1, (unsigned)(ns << a.h), 1, 1,
+                           (unsigned)LJ.total, (CUstream)st, params, nullptr) != CUDA_SUCCESS)
           return fail(TCX_E_CUDA, "cuLaunchKernel failed for " + jit_kernel_name(jit_pass, km));
         continue;
       }

@@ -108,7 +108,7 @@ def test_grad_random_circuits(tc, dtype, seed, jit):
 
 @pytest.mark.parametrize("jit", [True, False])
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
-@pytest.mark.parametrize("n,t,seed", [(12, 7, 0), (14, 8, 1), (13, 6, 2)])
+@pytest.mark.parametrize("n,t,seed", [(12, 7, 0), (14, 8, 1), (13, 6, 2), (16, 8, 3)])
 def test_grad_multi_pass_random(tc, dtype, n, t, seed, jit):
     """Multi-pass forward, extra lambda passes, multi-pass backward, several tiles."""
     c = W.random_circuit(n, 90, 4000 + seed, n_params=6)
