@@ -280,7 +280,8 @@ def main():
                      "share_of_step": kms / total_k,
                      "peak_source": alu_src if roof["bound"] == "alu" else peak_src + " (MEASURED_PEAKS.json hbm_gbs)",
                      "hbm_achieved_gbs": byt / (kms / 1e3) / 1e9,
-                     "traffic": load_traffic(args.config, dom, cnt, args.steps)})
+                     "traffic": load_traffic(name, dom),
+                     "algorithmic_bytes_per_launch": byt / cnt})
     kernel_split = {k: {"ms": v[0] / args.steps, "launches_per_step": v[3] / args.steps,
                         "tflops": v[1] / max(v[0], 1e-9) / 1e9, "gbs": v[2] / max(v[0], 1e-9) / 1e6}
                     for k, v in by.items()}
@@ -327,13 +328,13 @@ def main():
     return 0
 
 
-def load_traffic(cfg, phase, launches, steps):
-    """DRAM traffic per launch of the dominant kernel from a committed ncu capture
-    (profiles/traffic.json, written from `ncu --set full`), else None."""
+def load_traffic(workload, phase):
+    """DRAM bytes per launch of the dominant kernel class from a committed ncu capture
+    (profiles/traffic.json via tools/summarize_profile.py), else None."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             d = json.load(f)
-        return d.get(f"cfg{cfg}", {}).get(phase)
+        return d.get(workload, {}).get(phase)
     except Exception:
         return None
 

@@ -441,6 +441,48 @@ uint32_t swizzle_bit(int p, bool c128) {
   return (1u << p) ^ (c128 ? col128[p - lg] : col64[p - lg]);
 }
 
+TmaDims tma_dims(int n, uint64_t wmask, bool c128) {
+  TmaDims d{};
+  d.epa = c128 ? 2 : 1;
+  // element-index bits: for complex128 bit 0 is the (re,im)-half, inside the window
+  const int eb = c128 ? 1 : 0;
+  std::vector<std::pair<int, int>> runs;  // (start element-bit, nbits), alternating in/out
+  std::vector<int> in;
+  int bit = 0;
+  const int nbits = n + eb;
+  auto win = [&](int e) { return e < eb ? true : ((wmask >> (e - eb)) & 1) != 0; };
+  while (bit < nbits) {
+    const bool w = win(bit);
+    int len = 0;
+    while (bit + len < nbits && win(bit + len) == w) ++len;
+    // window runs longer than 8 bits split (box dims <= 256)
+    for (int o = 0; o < len;) {
+      int l = w ? std::min(8, len - o) : len - o;
+      runs.push_back({bit + o, l});
+      in.push_back(w ? 1 : 0);
+      o += l;
+    }
+    bit += len;
+  }
+  // batch: merged into a trailing out-of-window run, else its own dim
+  if (in.back() == 0) {
+    runs.back().second = -1;
+  } else {
+    runs.push_back({nbits, -1});
+    in.push_back(0);
+  }
+  if (runs.size() > 5) return d;  // rank 0: not expressible as one box
+  d.rank = (int)runs.size();
+  for (int i = 0; i < d.rank; ++i) {
+    d.start[i] = runs[i].first;
+    d.bits[i] = runs[i].second;
+    d.inwin[i] = in[i];
+  }
+  // innermost box >= 16 bytes
+  if (!d.inwin[0] || (1 << d.bits[0]) * 8 < 16) d.rank = 0;
+  return d;
+}
+
 tcx_status build_pauli(int n, int T, const uint8_t* codes, const double* w, Pauli& p,
                        std::string& err) {
   if (n < 1 || n > kMaxQubits) {
@@ -454,6 +496,14 @@ tcx_status build_pauli(int n, int T, const uint8_t* codes, const double* w, Paul
   p.n = n;
   p.codes.assign(codes, codes + (size_t)T * n);
   p.weights.assign(w, w + T);
+  uint64_t h = 1469598103934665603ull ^ (uint64_t)n;
+  auto mix = [&](const void* d, size_t len) {
+    const unsigned char* c = (const unsigned char*)d;
+    for (size_t i = 0; i < len; ++i) h = (h ^ c[i]) * 1099511628211ull;
+  };
+  mix(p.codes.data(), p.codes.size());
+  mix(p.weights.data(), p.weights.size() * sizeof(double));
+  p.hash = h;
   for (int j = 0; j < T; ++j) {
     if (!std::isfinite(w[j])) {
       err = "pauli: term " + std::to_string(j) + " has a non-finite weight";
@@ -548,8 +598,9 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
   P.tpc = (int)std::min<int64_t>(64, std::max<int64_t>(1, P.tiles / 32));
   // two lock-stepped sub-tiles (512 threads) share one instruction stream in the JIT
   // kernels when tiles pair up and a sub-tile has whole warps
-  P.jit_nsub = (P.tpc % 2 == 0 && P.h >= 5) ? 2 : 1;
-  if (const char* e = getenv("TCX_JIT_NSUB")) P.jit_nsub = std::max(1, std::min(P.jit_nsub, atoi(e)));
+  P.jit_nsub = 1;  // 2 = lock-stepped sub-tiles (measured slower with FFMA2 code; opt-in via TCX_JIT_NSUB)
+  if (const char* e = getenv("TCX_JIT_NSUB"))
+    if (atoi(e) == 2 && P.tpc % 2 == 0 && P.h >= 5) P.jit_nsub = 2;
   // ---- lower
   int pos[kMaxQubits];
   for (int q = 0; q < n; ++q) pos[q] = n - 1 - q;  // PAPER.md:249 qubit 0 = MSB

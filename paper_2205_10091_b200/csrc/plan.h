@@ -97,6 +97,7 @@ struct Pauli {
   int n = 0;
   std::vector<uint8_t> codes;  // [T][n]
   std::vector<double> weights;
+  uint64_t hash = 0;           // content hash (binding cache key; handles may be reused)
 };
 
 // Lambda evaluation unit: a window pass computing some Pauli groups.
@@ -158,9 +159,21 @@ struct Plan {
   std::mutex jit_mu;
 
   std::mutex mu;
-  std::map<const void*, std::shared_ptr<Binding>> bindings;
+  std::map<uint64_t, std::shared_ptr<Binding>> bindings;  // keyed by Pauli::hash
   std::map<int, std::shared_ptr<DeviceTables>> dev;
 };
+
+// TMA view of a pass window: the state [B][2^n] of 8-byte elements
+// (complex64 = 1, complex128 = 2 per amplitude) as a rank <= 5 tensor whose dims are the
+// runs of window / non-window index bits; the box is the tile (window dims full, others 1).
+struct TmaDims {
+  int rank = 0;         // 0: the window does not fit a rank-5 box (plain loads are used)
+  int start[5];         // first element-index bit of each dim (element = amp * epa + half)
+  int bits[5];          // dim size 2^bits (the last dim also spans the batch: bits = -1)
+  int inwin[5];         // 1: dim lies inside the window (box = full dim)
+  int epa;              // 8-byte elements per amplitude
+};
+TmaDims tma_dims(int n, uint64_t wmask, bool c128);
 
 // Build; returns TCX_OK or an error with message.
 tcx_status build_plan(int n, int P, const tcx_gate* gates, int64_t G, const double* mats,

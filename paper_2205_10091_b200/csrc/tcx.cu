@@ -295,6 +295,10 @@ struct Drv {
   CUresult (*launchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
                            unsigned, CUstream, void**, void**);
   CUresult (*funcSetAttribute)(CUfunction, CUfunction_attribute, int);
+  CUresult (*tensorMapEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 };
 Drv& drv() {
   static Drv D;
@@ -308,9 +312,34 @@ Drv& drv() {
     D.ok = get("cuModuleLoadData", (void**)&D.moduleLoadData) &&
            get("cuModuleGetFunction", (void**)&D.moduleGetFunction) &&
            get("cuLaunchKernel", (void**)&D.launchKernel) &&
-           get("cuFuncSetAttribute", (void**)&D.funcSetAttribute);
+           get("cuFuncSetAttribute", (void**)&D.funcSetAttribute) &&
+           get("cuTensorMapEncodeTiled", (void**)&D.tensorMapEncodeTiled);
   });
   return D;
+}
+
+// Tensor map of a [B][2^n] state buffer viewed through a pass window (plan.cpp tma_dims):
+// 8-byte elements, box = one tile, no swizzle (the kernels read the dense tile in the
+// load/store thread mapping, which is bank-conflict free).
+bool encode_tmap(void* out, void* base, const TmaDims& td, int n, int64_t B) {
+  Drv& D = drv();
+  if (!D.ok || td.rank == 0 || !base) return false;
+  cuuint64_t dims[5], strides[4];
+  cuuint32_t box[5], estr[5];
+  const uint64_t total = (uint64_t)B << n;  // amplitudes
+  for (int d = 0; d < td.rank; ++d) {
+    const uint64_t elems = total * (uint64_t)td.epa;
+    dims[d] = td.bits[d] >= 0 ? (1ull << td.bits[d]) : (elems >> td.start[d]);
+    box[d] = td.inwin[d] ? (cuuint32_t)(1u << td.bits[d]) : 1u;
+    estr[d] = 1;
+    if (d > 0) strides[d - 1] = (1ull << td.start[d]) * 8ull;
+    if (dims[d] == 0 || dims[d] > (1ull << 32)) return false;
+  }
+  CUtensorMap* m = reinterpret_cast<CUtensorMap*>(out);
+  return D.tensorMapEncodeTiled(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, (cuuint32_t)td.rank, base, dims,
+                                strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 tcx_status device_tables(Plan& P, DeviceTables*& out) {
@@ -398,17 +427,17 @@ struct BindDev {
 tcx_status binding_for(Plan& P, const tcx_pauli* H, std::shared_ptr<Binding>& out, BindDev* dv) {
   {
     std::lock_guard<std::mutex> lk(P.mu);
-    auto it = P.bindings.find(H);
+    auto it = P.bindings.find(H->p.hash);
     if (it != P.bindings.end()) out = it->second;
   }
   if (!out) {
     auto b = bind(P, H->p);
     std::lock_guard<std::mutex> lk(P.mu);
-    auto it = P.bindings.find(H);
+    auto it = P.bindings.find(H->p.hash);
     if (it != P.bindings.end())
       out = it->second;
     else
-      P.bindings[H] = out = b;
+      P.bindings[H->p.hash] = out = b;
   }
   if (!out->xmask_ok) return fail(TCX_E_UNSUPPORTED, out->err);
   if (dv) {
@@ -620,6 +649,13 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
       if (jf) {
         Drv& D = drv();
         const int ns = P.jit_nsub;
+        if (b0 == 0) {
+          const TmaDims td = tma_dims(P.n, a.wmask, c128);
+          a.use_tma = 0;
+          if (td.rank > 0 && ns == 1 && encode_tmap(a.tmap[0], a.psi, td, P.n, B))
+            a.use_tma = (wl.lam == 0 || encode_tmap(a.tmap[1], a.lam, td, P.n, B)) ? 1 : 0;
+          if (!(a.mode & (M_LOAD_PSI | M_LOAD_LAM | M_STORE_PSI | M_STORE_LAM))) a.use_tma = 0;
+        }
         const SmemLayout LJ = smem_layout(a.t, a.h, rs, a.mat_count, a.max_stage_acc,
                                           (a.mode & M_BWD) ? a.acc_count : 0, a.nstages, two, ns);
         if (LJ.total > 227 * 1024 - 256)
