@@ -122,7 +122,8 @@ def run_reference(args, rank, world):
     value = rows * args.steps / total
     unit = "circuits/s"
     line = {
-        "metric": "batched <H>+grad circuits/s (%s)" % name, "value": value, "unit": unit,
+        "metric": ("batched <H>+grad circuits/s (%s)" if mode == "grad" else
+                   "batched <H> circuits/s (%s, forward only)") % name, "value": value, "unit": unit,
         "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -148,6 +149,8 @@ def main():
     ap.add_argument("--tile-bits", type=int, default=0)
     ap.add_argument("--max-ops-per-pass", type=int, default=0)
     ap.add_argument("--jit", type=int, default=1, help="1: per-circuit specialised kernels")
+    ap.add_argument("--mode", default=None, choices=["grad", "expect"],
+                    help="grad (E + adjoint gradient, default) or expect (forward + E only; cfg4)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-rows", type=int, default=8)
     ap.add_argument("--cpu-rows", type=int, default=8)
@@ -179,7 +182,8 @@ def main():
                     jit=bool(args.jit))
     P = tcx.Pauli(H)
     t_jit = time.perf_counter()
-    C.compile(P, B=B, kind="grad")  # the K.jit analog: excluded from timings
+    mode = args.mode or ("expect" if circ.n_params == 0 else "grad")
+    C.compile(P, B=B, kind=mode)  # the K.jit analog: excluded from timings
     t_jit = time.perf_counter() - t_jit
     info = C.info(P)
     th = torch.as_tensor(np.ascontiguousarray(theta)).to(dev)
@@ -192,8 +196,12 @@ def main():
     from paper_2205_10091_b200.dist import allreduce_loss_grad
 
     def step():
-        tcx.grad_batch(C, P, th, stream=stream, ws=ws, out=(E, G))
-        allreduce_loss_grad(E, G[:, :circ.n_params], out=red)
+        if mode == "grad":
+            tcx.grad_batch(C, P, th, stream=stream, ws=ws, out=(E, G))
+            allreduce_loss_grad(E, G[:, :circ.n_params], out=red)
+        else:
+            Ex = tcx.expect_batch(C, P, th, stream=stream, ws=ws)
+            allreduce_loss_grad(Ex, G[:, :0], out=red[:1])
 
     for _ in range(args.warmup):
         step()
@@ -230,8 +238,12 @@ def main():
     ws2 = tcx.Workspace()
 
     def e2e_step():
-        tcx.grad_batch_host(C, P, th_h.numpy(), E_h.numpy(), G_h.numpy(), stream=stream, ws=ws2,
-                            device=dev)
+        if mode == "grad":
+            tcx.grad_batch_host(C, P, th_h.numpy(), E_h.numpy(), G_h.numpy(), stream=stream,
+                                ws=ws2, device=dev)
+        else:
+            tcx.expect_batch_host(C, P, th_h.numpy(), E_h.numpy(), stream=stream, ws=ws2,
+                                  device=dev)
     e2e_step()
     if world > 1:
         dist.barrier()
@@ -294,9 +306,10 @@ def main():
         cpu = {"value": rows / secs, "unit": "circuits/s", "cores": rows, "kind": "oracle",
                "sample": f"{rows} theta rows of {name} (one OpenMP thread per row), {secs:.1f} s"}
 
-    launches = C.launch_count(P, B, True) * args.steps
+    launches = C.launch_count(P, B, mode == "grad") * args.steps
     line = {
-        "metric": "batched <H>+grad circuits/s (%s)" % name,
+        "metric": ("batched <H>+grad circuits/s (%s)" if mode == "grad" else
+                   "batched <H> circuits/s (%s, forward only)") % name,
         "value": value, "unit": "circuits/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "c64" if dtype == "c64" else "c128",
@@ -310,13 +323,14 @@ def main():
                    "plan": {k: info[k] for k in ("tile_bits", "reg_bits", "fwd_passes",
                                                  "lambda_passes", "bwd_passes", "stages",
                                                  "n_ops", "jit")},
-                   "jit_compile_s": round(t_jit, 2)},
+                   "jit_compile_s": round(t_jit, 2), "mode": mode,
+                   "max_ops_per_pass": args.max_ops_per_pass},
         "roofline": roof,
         "kernels": kernel_split,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "circuits/s",
                 "h2d_bytes_per_step": int(B * circ.n_params * 8),
-                "d2h_bytes_per_step": int(B * 8 + B * circ.n_params * 8)},
+                "d2h_bytes_per_step": int(B * 8 + (B * circ.n_params * 8 if mode == "grad" else 0))},
         "gpu_launches": int(launches),
         "clocks": clk,
     }

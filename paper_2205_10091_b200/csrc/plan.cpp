@@ -921,6 +921,7 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
 // ---------------------------------------------------------------- binding
 std::shared_ptr<Binding> bind(Plan& P, const Pauli& H) {
   auto B = std::make_shared<Binding>();
+  B->hash = H.hash;
   const int n = P.n, t = P.t, c = P.c;
   // group terms by X/Y flip mask (physical bits through the final layout)
   std::map<uint64_t, std::vector<KPTerm>> groups;

@@ -109,6 +109,7 @@ struct LamUnit {
 };
 
 struct Binding {        // (circuit, pauli) specific lambda schedule
+  uint64_t hash = 0;    // Pauli::hash this binding was built from
   std::vector<KGroup> groups;
   std::vector<KPTerm> pterms;
   std::vector<LamUnit> units;
@@ -120,9 +121,8 @@ struct Binding {        // (circuit, pauli) specific lambda schedule
 
 struct DeviceTables;
 
-struct JitKernel {      // NVRTC-compiled specialisation of one pass (jit.cpp)
-  int pass = 0, km = 0; // km: 0 forward, 1 backward, 2 fused single pass
-  std::string name;
+struct JitKernel {      // NVRTC-compiled specialisation (jit.cpp)
+  std::string key, name;
   std::vector<char> cubin;
 };
 
@@ -154,7 +154,7 @@ struct Plan {
   int jit_nsub = 1;              // lock-stepped sub-tiles per CTA in JIT kernels
 
   bool jit_on = false;             // per-circuit specialised kernels (compiled lazily)
-  std::map<int, JitKernel> jit;    // key pass*4 + km -> compiled CUBIN
+  std::map<std::string, JitKernel> jit;  // key (jit.h) -> compiled CUBIN
   std::string jit_note;            // why JIT is off, if it is
   std::mutex jit_mu;
 

@@ -265,8 +265,8 @@ struct DevBuf {
 namespace tcx {
 struct DeviceTables {
   DevBuf kops, kterms, kstages, mitems, dcons, gitems, pptr, plist, fixed, layout, swb;
-  std::map<int, CUfunction> jit;    // key pass*4 + km
-  std::map<int, size_t> jit_smem;   // dynamic smem opted in per function
+  std::map<std::string, CUfunction> jit;   // key (jit.h)
+  std::map<std::string, size_t> jit_smem;  // dynamic smem opted in per function
 };
 }  // namespace tcx
 
@@ -371,7 +371,7 @@ tcx_status device_tables(Plan& P, DeviceTables*& out) {
 
 // Specialised kernel for (pass, km): compiled (NVRTC / disk cache) and loaded into this
 // device's context on first use.  Returns nullptr when the plan runs generic kernels.
-tcx_status jit_function(Plan& P, DeviceTables* DT, int key, CUfunction* f) {
+tcx_status jit_function(Plan& P, DeviceTables* DT, const std::string& key, CUfunction* f) {
   *f = nullptr;
   if (!P.jit_on) return TCX_OK;
   {
@@ -402,17 +402,19 @@ tcx_status jit_function(Plan& P, DeviceTables* DT, int key, CUfunction* f) {
 }
 
 // Compile every specialised kernel a call of this kind needs, in parallel, before launching.
-tcx_status jit_prepare(Plan& P, int kind, bool mega) {
+tcx_status jit_prepare(Plan& P, int kind, bool mega, const Binding* Bd) {
   if (!P.jit_on) return TCX_OK;
-  std::vector<int> keys;
+  std::vector<std::string> keys;
   const int nP = (int)P.passes.size();
   if (mega) {
-    keys.push_back(kind == 1 ? 2 : 0);
+    keys.push_back(jit_key_pass(0, kind == 1 ? 2 : 0));
   } else {
     for (int p = 0; p < nP; ++p) {
-      keys.push_back(p * 4 + 0);
-      if (kind == 1) keys.push_back(p * 4 + 1);
+      keys.push_back(jit_key_pass(p, 0));
+      if (kind == 1) keys.push_back(jit_key_pass(p, 1));
     }
+    if (Bd)
+      for (int u = 1; u < (int)Bd->units.size(); ++u) keys.push_back(jit_key_lambda(Bd->hash, u));
   }
   std::string err;
   if (!jit_build(P, keys, err)) return fail(TCX_E_CUDA, err);
@@ -558,7 +560,7 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
   if (ws_bytes < wl.total)
     return fail(TCX_E_INVALID, "workspace too small: need " + std::to_string(wl.total) +
                                    " bytes, got " + std::to_string(ws_bytes));
-  if ((s = jit_prepare(P, kind, wl.mega))) return s;
+  if ((s = jit_prepare(P, kind, wl.mega, Bd.get()))) return s;
   char* W = (char*)ws;
   const bool c128 = P.dtype == TCX_C128;
   const int rs = c128 ? 8 : 4;
@@ -623,7 +625,7 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
     a.max_stage_acc = p.max_stage_acc;
     a.last_is_top = p.last_is_top;
   };
-  auto launch_raw = [&](PassArgs& a, int jit_pass) -> tcx_status {
+  auto launch_raw = [&](PassArgs& a, const std::string& jkey) -> tcx_status {
     const bool fwd = (a.mode & (M_FWD | M_LAMBDA)) != 0;
     const bool two = (a.mode & M_BWD) != 0;
     const int km = (fwd && two) ? KM_MEGA : (two ? KM_BWD : KM_FWD);
@@ -637,9 +639,8 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
     if (L.total > 227 * 1024 - 256)
       return fail(TCX_E_UNSUPPORTED, "pass needs " + std::to_string(L.total) +
                                          " B of shared memory (> 227 KB); lower tile_bits");
-    CUfunction jf = nullptr;  // specialised kernel for this pass and mode
-    const int jkey = jit_pass * 4 + km;
-    if (jit_pass >= 0) {
+    CUfunction jf = nullptr;  // specialised kernel for this pass / lambda unit and mode
+    if (!jkey.empty()) {
       tcx_status js = jit_function(P, DT, jkey, &jf);
       if (js) return js;
     }
@@ -658,18 +659,18 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
         }
         const SmemLayout LJ = smem_layout(a.t, a.h, rs, a.mat_count, a.max_stage_acc,
                                           (a.mode & M_BWD) ? a.acc_count : 0, a.nstages, two, ns);
-        if (LJ.total > 227 * 1024 - 256)
+        if (LJ.total > 227 * 1024 - 1280)
           return fail(TCX_E_UNSUPPORTED, "JIT pass needs too much shared memory");
         if (LJ.total > 48 * 1024 && (size_t)LJ.total > DT->jit_smem[jkey]) {
           if (D.funcSetAttribute(jf, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, LJ.total) !=
               CUDA_SUCCESS)
-            return fail(TCX_E_CUDA, "cuFuncSetAttribute failed for " + jit_kernel_name(jit_pass, km));
+            return fail(TCX_E_CUDA, "cuFuncSetAttribute failed for " + jit_kernel_name(jkey));
           DT->jit_smem[jkey] = LJ.total;
         }
         void* params[] = {&a};
         if (D.launchKernel(jf, (unsigned)S, (unsigned)rows, 1, (unsigned)(ns << a.h), 1, 1,
                            (unsigned)LJ.total, (CUstream)st, params, nullptr) != CUDA_SUCCESS)
-          return fail(TCX_E_CUDA, "cuLaunchKernel failed for " + jit_kernel_name(jit_pass, km));
+          return fail(TCX_E_CUDA, "cuLaunchKernel failed for " + jit_kernel_name(jkey));
         continue;
       }
       cudaError_t e;
@@ -687,14 +688,21 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
   };
   const double Nf = (double)((int64_t)1 << P.n), csz = 2.0 * rs, Bf = (double)B;
   auto launch = [&](PassArgs& a, int phase, int index, double flops_amp) -> tcx_status {
-    const int jit_pass = (phase == 1 || phase == 3 || phase == 5) ? index : -1;
+    std::string jkey;
+    if (P.jit_on) {
+      const bool fwdk = (a.mode & (M_FWD | M_LAMBDA)) != 0, bwdk = (a.mode & M_BWD) != 0;
+      if (phase == 1 || phase == 3 || phase == 5)
+        jkey = jit_key_pass(index, (fwdk && bwdk) ? 2 : (bwdk ? 1 : 0));
+      else if (phase == 2 && Bd)
+        jkey = jit_key_lambda(Bd->hash, index);
+    }
     ProfEntry pe{};
     if (g_prof.on) {
       CUDA_TRY(cudaEventCreate(&pe.a));
       CUDA_TRY(cudaEventCreate(&pe.b));
       CUDA_TRY(cudaEventRecord(pe.a, st));
     }
-    tcx_status r0 = launch_raw(a, jit_pass);
+    tcx_status r0 = launch_raw(a, jkey);
     if (r0) return r0;
     if (g_prof.on) {
       CUDA_TRY(cudaEventRecord(pe.b, st));
@@ -977,7 +985,7 @@ tcx_status tcx_circuit_jit(const tcx_circuit* circ, const tcx_pauli* pauli, int6
     if (s) return s;
   }
   WsLayout wl = ws_layout(P, Bd.get(), B, kind, false);
-  return jit_prepare(P, kind, wl.mega);
+  return jit_prepare(P, kind, wl.mega, Bd.get());
 }
 
 tcx_status tcx_circuit_info(const tcx_circuit* circ, const tcx_pauli* pauli, tcx_plan_info* o) {

@@ -322,3 +322,20 @@ def profile_read(cap: int = 1 << 16):
     _check(_lib.tcx_profile_read(arr, cap, ctypes.byref(n)))
     return [(PHASES[arr[i].phase], arr[i].index, arr[i].ms, arr[i].flops, arr[i].bytes)
             for i in range(n.value)]
+
+
+def expect_batch_host(circ: Circuit, pauli: Pauli, theta_host: np.ndarray, E_host=None,
+                      stream=None, ws: Workspace = None, device=None):
+    """End-to-end E through tcx_expect_batch_host (HOST buffers; copies inside)."""
+    torch = _torch()
+    B = theta_host.shape[0]
+    if E_host is None:
+        E_host = np.empty(B, dtype=np.float64)
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    buf, need = (ws or _default_ws).get(circ, pauli, B, WS_HOST_IO, dev)
+    th = theta_host if theta_host.size else np.zeros((B, 1))
+    _check(_lib.tcx_expect_batch_host(circ.h, pauli.h, ctypes.c_void_p(th.ctypes.data), B,
+                                      ctypes.c_void_p(E_host.ctypes.data),
+                                      ctypes.c_void_p(buf.data_ptr()), buf.numel(),
+                                      _stream_ptr(stream)))
+    return E_host
