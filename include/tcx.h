@@ -94,7 +94,10 @@ typedef struct {
     int32_t max_ops_per_pass; /* fusion depth cap: 0 = light-cone (unlimited), 1 = unfused */
     int32_t jit;            /* 0 = per-circuit specialised kernels (NVRTC, sm_100a) when
                                available, -1 = the precompiled generic kernels */
-    int32_t reserved[3];
+    int32_t global_bits;    /* g > 0: the state is sharded over 2^g ranks on its top g index
+                               bits (qubits 0..g-1); run with tcx_shard_* (north_star
+                               "shards on its top log2(G) global qubits") */
+    int32_t reserved[2];
 } tcx_build_opts;
 
 /* Executed-plan summary (for reports and tests). */
@@ -109,6 +112,8 @@ typedef struct {
     int32_t unitary;          /* 1 if every payload is unitary (grad allowed) */
     int32_t relabeled;        /* 1 if SWAP gates were applied as qubit relabels */
     int32_t jit;              /* 1 if the passes run per-circuit specialised kernels */
+    int32_t global_bits;      /* sharded: g (2^g ranks), else 0 */
+    int32_t segments;         /* sharded: forward segments (exchanges = segments - 1) */
     int64_t tiles_per_state;  /* 2^(n-t) */
     int64_t acc_slots;        /* gradient partial slots per tile */
     int64_t mat_reals;        /* per-theta materialised matrix entries */
@@ -192,6 +197,33 @@ tcx_status tcx_circuit_layout(const tcx_circuit* circ, int32_t* out);
 /* Kernel launches one tcx_grad_batch / tcx_expect_batch call enqueues for B rows. */
 tcx_status tcx_launch_count(const tcx_circuit* circ, const tcx_pauli* pauli, int64_t B,
                             int32_t want_grad, int32_t* launches);
+
+/* ---- Sharded single state (circuit built with tcx_build_opts.global_bits = g > 0) ----
+ * north_star: "A single large state shards on its top log2(G) global qubits, and gates on
+ * global qubits are handled by NCCL all-to-all qubit swaps."  Rank r (of G = 2^g) holds the
+ * 2^(n-g) amplitudes whose top g index bits equal r.  Diagonal phases and CNOT controls on
+ * global qubits are rank-dependent constants; a gate that needs a global qubit inside a
+ * window is preceded by an EXCHANGE of the g global bits with the top g local bits: every
+ * rank sends chunk k (the 2^(n-2g) amplitudes whose top local bits equal k, contiguous,
+ * per theta row) to rank k and receives chunk r from it -- an all-to-all the CALLER runs
+ * (NCCL via torch.distributed, or device copies between virtual ranks).
+ * The program is a fixed list of steps identical on all ranks; tcx_shard_exec enqueues
+ * one non-exchange step for one rank on the caller's stream; FINALIZE writes this rank's
+ * partial E[B] and grad[B][P], which the caller all-reduces (sum) over ranks. */
+enum { TCX_STEP_MATERIALIZE = 0, TCX_STEP_FWD = 1, TCX_STEP_LAMBDA = 2, TCX_STEP_BWD = 3,
+       TCX_STEP_FINALIZE = 4, TCX_STEP_EXCHANGE = 5 /* arg: 1 = psi, 3 = psi and lambda */ };
+typedef struct { int32_t kind, arg; } tcx_shard_step;
+tcx_status tcx_shard_program(const tcx_circuit* circ, const tcx_pauli* pauli, int32_t want_grad,
+                             tcx_shard_step* steps, int32_t cap, int32_t* n_steps);
+tcx_status tcx_shard_exec(const tcx_circuit* circ, const tcx_pauli* pauli, int32_t rank,
+                          int32_t want_grad, const tcx_shard_step* step, const double* theta,
+                          int64_t B, double* E_partial, double* grad_partial, void* ws,
+                          size_t ws_bytes, void* cuda_stream);
+/* Device pointers of this rank's psi / lambda ([B][2^(n-g)] complex) inside ws, for the
+ * caller's exchanges; local_amps = 2^(n-g). */
+tcx_status tcx_shard_buffers(const tcx_circuit* circ, const tcx_pauli* pauli, int64_t B,
+                             int32_t want_grad, void* ws, void** psi, void** lambda,
+                             int64_t* local_amps);
 
 /* Per-launch device timing (bench.py roofline).  When enabled on the calling thread,
  * every kernel a compute entry enqueues is bracketed by CUDA events recorded on the

@@ -68,6 +68,7 @@ enum { KM_FWD = 0, KM_BWD = 1, KM_MEGA = 2 };
 struct PassArgs {
   alignas(64) unsigned char tmap[2][128];  // CUtensorMap of psi / lambda (TMA tile I/O)
   int use_tma;                             // 1: tmap valid for this launch
+  uint64_t gbase;                          // sharded state: rank << n_local (else 0)
   void* psi;
   void* lam;
   const void* mats;

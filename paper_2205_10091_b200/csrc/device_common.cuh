@@ -18,7 +18,8 @@ template <int RB>
 struct Map {
   uint32_t sb;        // swizzled smem index of slot 0
   uint32_t so[RB];    // swizzle image of register bit k
-  uint64_t g;         // global physical index of slot 0
+  uint64_t g;         // physical index of slot 0 within this rank's (local) state
+  uint64_t gb;        // sharded states: this rank's global index bits (0 otherwise)
   uint32_t gp;        // physical bit positions of register bits, 6 bits each
 };
 template <int RB>
@@ -28,9 +29,10 @@ __device__ __forceinline__ int gpos(const Map<RB>& m, int k) {
 template <int RB>
 __device__ __forceinline__ void make_map(Map<RB>& m, const int8_t* R, const int8_t* T, int h,
                                          int tid, uint64_t outer, const int8_t* wpos,
-                                         const uint32_t* swb) {
+                                         const uint32_t* swb, uint64_t gb = 0) {
   m.sb = 0;
   m.g = outer;
+  m.gb = gb;
   for (int i = 0; i < h; ++i)
     if (tid >> i & 1) {
       const int l = T[i];
@@ -47,9 +49,10 @@ __device__ __forceinline__ void make_map(Map<RB>& m, const int8_t* R, const int8
 }
 template <int RB>
 __device__ __forceinline__ void make_top(Map<RB>& m, int h, int tid, uint64_t outer,
-                                         const int8_t* wpos, const uint32_t* swb) {
+                                         const int8_t* wpos, const uint32_t* swb, uint64_t gb = 0) {
   m.sb = 0;
   m.g = outer;
+  m.gb = gb;
   for (int i = 0; i < h; ++i)
     if (tid >> i & 1) {
       m.sb ^= swb[i];
@@ -418,7 +421,7 @@ template <typename Real, int RB, bool CONJ>
 __device__ __forceinline__ void diag_term(Cx<Real>* v, const Map<RB>& mp, const KTerm& tm,
                                           const Real* mats) {
   const Real cw = mats[tm.wofs], sw = mats[tm.wofs + 1];
-  const uint32_t tp = __popcll(mp.g & tm.mask) & 1u;
+  const uint32_t tp = __popcll((mp.g | mp.gb) & tm.mask) & 1u;
   const uint32_t mr = regmask<RB>(mp, tm.mask);
 #pragma unroll
   for (int j = 0; j < (1 << RB); ++j) {
@@ -439,7 +442,7 @@ __device__ __forceinline__ void op_fwd(const KOp& o, Cx<Real>* v, const Map<RB>&
     for (int i = 0; i < 8; ++i) m[i] = mats[o.mat + (sizeof(Real) == 4 ? 2 * i + 1 : i)];
     dispatch_slot<RB>(o.a, [&](auto K) { apply_u1<RB, decltype(K)::value>(v, m); });
   } else if (o.type == OP_CX) {
-    op_cx<RB>(o, v, mp.g);
+    op_cx<RB>(o, v, mp.g | mp.gb);
   } else if (o.type == OP_DIAG) {
     for (int k = 0; k < o.nterm; ++k) diag_term<Real, RB, false>(v, mp, terms[o.term + k], mats);
   }
@@ -464,8 +467,8 @@ __device__ __forceinline__ void op_bwd(const KOp& o, Cx<Real>* v, Cx<Real>* l,
       apply_u1_dag<RB, k>(l, m);
     });
   } else if (o.type == OP_CX) {
-    op_cx<RB>(o, v, mp.g);
-    op_cx<RB>(o, l, mp.g);
+    op_cx<RB>(o, v, mp.g | mp.gb);
+    op_cx<RB>(o, l, mp.g | mp.gb);
   } else if (o.type == OP_DIAG) {
     // gradient: Im(conj(lambda) Z_mask psi) at the op output (all terms commute);
     // Im(conj(l) v) is invariant under the common phase, so order is free.
@@ -482,7 +485,7 @@ __device__ __forceinline__ void op_bwd(const KOp& o, Cx<Real>* v, Cx<Real>* l,
           cur = tm.acc;
           acc = 0;
         }
-        const uint32_t tp = __popcll(mp.g & tm.mask) & 1u;
+        const uint32_t tp = __popcll((mp.g | mp.gb) & tm.mask) & 1u;
         const uint32_t mr = regmask<RB>(mp, tm.mask);
 #pragma unroll
         for (int j = 0; j < (1 << RB); ++j) {
@@ -529,7 +532,7 @@ __device__ __forceinline__ Real lambda_tile(const PassArgs& a, Cx<Real>* v, Cx<R
     for (int j = 0; j < NR; ++j) cr[j] = ci[j] = 0;
     for (int k = 0; k < G.term_count; ++k) {
       const KPTerm pt = a.pterms[G.term_begin + k];
-      const uint32_t tp = __popcll(top.g & pt.zy) & 1u;
+      const uint32_t tp = __popcll((top.g | top.gb) & pt.zy) & 1u;
       const uint32_t mr = regmask<RB>(top, pt.zy);
       const Real re = (Real)pt.cre, im = (Real)pt.cim;
 #pragma unroll

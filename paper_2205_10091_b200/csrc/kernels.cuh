@@ -79,12 +79,12 @@ __global__ void __launch_bounds__(256, 2) pass_kernel(const PassArgs a) {
         }
     }
     Map<RB> top;
-    make_top<RB>(top, h, tid, outer, s_wpos, s_swb);
+    make_top<RB>(top, h, tid, outer, s_wpos, s_swb, a.gbase);
     C v[NR], l[NR];
     if (mode & M_INIT) {
 #pragma unroll
       for (int j = 0; j < NR; ++j) {
-        v[j].x = gidx(top, j) == 0 ? Real(1) : Real(0);
+        v[j].x = (gidx(top, j) | a.gbase) == 0 ? Real(1) : Real(0);
         v[j].y = 0;
       }
     } else if (mode & M_LOAD_PSI) {
@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(256, 2) pass_kernel(const PassArgs a) {
         const KStage& st = sst[s];
         if (s > 0 && !st.same_as_prev) {
           Map<RB> nx;
-          make_map<RB>(nx, st.R, st.T, h, tid, outer, s_wpos, s_swb);
+          make_map<RB>(nx, st.R, st.T, h, tid, outer, s_wpos, s_swb, a.gbase);
           __syncthreads();
 #pragma unroll
           for (int j = 0; j < NR; ++j) xp[sidx(cur, j)] = v[j];
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(256, 2) pass_kernel(const PassArgs a) {
         const KStage& st = sst[s];
         const bool same = (s == a.nstages - 1) ? (a.last_is_top != 0) : (sst[s + 1].same_as_prev != 0);
         Map<RB> nx = cur;
-        if (!same) make_map<RB>(nx, st.R, st.T, h, tid, outer, s_wpos, s_swb);
+        if (!same) make_map<RB>(nx, st.R, st.T, h, tid, outer, s_wpos, s_swb, a.gbase);
         __syncthreads();
         if (pending >= 0) {
           const KStage& ps = sst[pending];

@@ -203,9 +203,11 @@ struct Scheduler {
   std::vector<char> done;
   int first = 0;
   uint64_t full;
+  int nl;  // local index bits (windows live there; sharded states keep the top bits global)
   Budget pass_budget;
   explicit Scheduler(Plan& p) : P(p), done(p.ops.size(), 0) {
     full = (P.n >= 64) ? ~0ull : ((1ull << P.n) - 1);
+    nl = P.nloc;
   }
   // light-cone closure under tile mask W (physical)
   double closure(uint64_t W, std::vector<int>* out) {
@@ -248,8 +250,8 @@ struct Scheduler {
     return 0;
   }
   uint64_t choose_window() {
-    const int n = P.n, t = P.t, c = P.c;
-    if (n <= t) return full;
+    const int n = nl, t = P.t, c = P.c;
+    if (n <= t) return (n >= 64) ? ~0ull : ((1ull << n) - 1);
     const uint64_t base = (1ull << c) - 1;
     uint64_t bestW = 0;
     double best = -1;
@@ -300,8 +302,9 @@ struct Scheduler {
     // (b) earliest-need-first
     {
       uint64_t W = base;
+      const uint64_t lmask = (n >= 64) ? ~0ull : ((1ull << n) - 1);
       for (int i = first; i < (int)P.ops.size() && popc64(W) < t; ++i) {
-        if (done[i]) continue;
+        if (done[i] || (P.ops[i].need & ~lmask)) continue;  // global bits never enter a window
         uint64_t nw = W | P.ops[i].need;
         if (popc64(nw) <= t) W = nw;
       }
@@ -519,11 +522,39 @@ tcx_status build_pauli(int n, int T, const uint8_t* codes, const double* w, Paul
   return TCX_OK;
 }
 
+namespace {
+uint64_t remap_mask(uint64_t m, const int* perm, int n) {
+  uint64_t r = 0;
+  for (int b = 0; b < n; ++b)
+    if (m >> b & 1) r |= 1ull << perm[b];
+  return r;
+}
+void remap_op(Op& o, const int* perm, int n) {
+  o.bits = remap_mask(o.bits, perm, n);
+  o.need = remap_mask(o.need, perm, n);
+  if (o.b0 >= 0) o.b0 = perm[o.b0];
+  if (o.b1 >= 0) o.b1 = perm[o.b1];
+  for (auto& t : o.terms) t.mask = remap_mask(t.mask, perm, n);
+}
+}  // namespace
+
+// Sharded layout exchange: global bits L+i <-> top local bits L-g+i (i < g), so each rank's
+// outgoing data for rank k is the contiguous chunk whose top local bits equal k.
+void shard_swap_perm(int n, int g, int* perm) {
+  const int L = n - g;
+  for (int b = 0; b < n; ++b) perm[b] = b;
+  for (int i = 0; i < g; ++i) {
+    perm[L + i] = L - g + i;
+    perm[L - g + i] = L + i;
+  }
+}
+
 tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const double* mats,
                       int64_t nmat, tcx_dtype dtype, const tcx_build_opts* opts, Plan& P,
                       std::string& err) {
-  if (n < 1 || n > 34) {
-    err = "n_qubits must be in [1, 34]";
+  const int gb_req = opts ? std::max(0, opts->global_bits) : 0;
+  if (n < 1 || n - gb_req > 34 || n > kMaxQubits) {
+    err = "n_qubits must be in [1, 34] per rank (n - global_bits <= 34)";
     return TCX_E_INVALID;
   }
   if (Pn < 0 || G < 0 || (G > 0 && !gates) || nmat < 0 || (nmat > 0 && !mats)) {
@@ -571,11 +602,18 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
   }
   // ---- options
   const bool c128 = dtype == TCX_C128;
+  const int gb = opts ? std::max(0, opts->global_bits) : 0;
+  if (gb > 0 && (gb > 6 || n - gb < 2 * gb + 2)) {
+    err = "global_bits must be in [1, 6] with n - g >= 2g + 2 local bits";
+    return TCX_E_INVALID;
+  }
+  P.gbits = gb;
+  P.nloc = n - gb;
   int tdef = c128 ? 11 : 12;
   int t = opts && opts->tile_bits > 0 ? opts->tile_bits : tdef;
   int c = opts && opts->coalesce_bits > 0 ? opts->coalesce_bits : (c128 ? 2 : 3);
   t = std::min(t, kMaxTileBits);
-  if (t >= n) t = n;
+  if (t >= n - gb) t = n - gb;
   int r = opts && opts->reg_bits > 0 ? opts->reg_bits : (t < tdef ? 3 : 4);
   r = std::min(r, kMaxRegBits);
   if (r > t) r = t;
@@ -585,7 +623,7 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
     return TCX_E_INVALID;
   }
   if (c > t) c = t;
-  if (n > t && t - c < 2) {
+  if (n - gb > t && t - c < 2) {
     err = "tile_bits - coalesce_bits must be >= 2";
     return TCX_E_INVALID;
   }
@@ -594,7 +632,7 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
   P.c = c;
   P.h = t - r;
   P.max_ops_per_pass = opts ? std::max(0, opts->max_ops_per_pass) : 0;
-  P.tiles = 1ll << (n - t);
+  P.tiles = 1ll << (n - gb - t);
   P.tpc = (int)std::min<int64_t>(64, std::max<int64_t>(1, P.tiles / 32));
   // two lock-stepped sub-tiles (512 threads) share one instruction stream in the JIT
   // kernels when tiles pair up and a sub-tile has whole warps
@@ -699,15 +737,31 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
   S.pass_budget.accs = 2048;
   S.pass_budget.ops = P.max_ops_per_pass;
   size_t left = P.ops.size();
+  int seg = 0;
+  bool swapped_last = false;
   while (left > 0) {
     uint64_t W = S.choose_window();
     std::vector<int> list;
     S.closure(W, &list);
-    if (list.empty()) {
-      err = "internal scheduler error (no progress)";
-      return TCX_E_INVALID;
+    if (list.empty() && gb > 0 && !swapped_last) {
+      // blocked on global qubits: exchange global <-> top-local bits, relabel what is left
+      int perm[64];
+      shard_swap_perm(n, gb, perm);
+      for (size_t i = 0; i < P.ops.size(); ++i)
+        if (!S.done[i]) remap_op(P.ops[i], perm, n);
+      for (int q = 0; q < n; ++q) pos[q] = perm[pos[q]];
+      ++seg;
+      swapped_last = true;
+      continue;
     }
+    if (list.empty()) {
+      err = gb > 0 ? "sharded schedule stuck (a 4x4 payload spans a global and a top-local qubit)"
+                   : "internal scheduler error (no progress)";
+      return gb > 0 ? TCX_E_UNSUPPORTED : TCX_E_INVALID;
+    }
+    swapped_last = false;
     PassInfo pi;
+    pi.seg = seg;
     pi.wmask = W;
     int l = 0;
     for (int b = 0; b < n; ++b)
@@ -721,12 +775,15 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
     left -= list.size();
     P.passes.push_back(std::move(pi));
   }
-  if (P.passes.empty()) {  // empty circuit: one init pass
+  if (P.passes.empty() || P.passes.back().seg != seg) {  // init / trailing-layout pass
     PassInfo pi;
+    pi.seg = seg;
     pi.wmask = (t >= 64) ? ~0ull : ((1ull << t) - 1);
     for (int l = 0; l < t; ++l) pi.W[l] = l;
     P.passes.push_back(pi);
   }
+  P.nseg = seg + 1;
+  for (int q = 0; q < n; ++q) P.layout[q] = pos[q];
 
   // ---- stages, kernel tables, matrix and accumulator layout
   int mat = 0, acc = 0;
@@ -949,14 +1006,19 @@ std::shared_ptr<Binding> bind(Plan& P, const Pauli& H) {
   }
   // units: the last forward pass, then greedy windows for the remaining groups
   std::vector<std::pair<uint64_t, std::vector<KPTerm>>> left(groups.begin(), groups.end());
-  const uint64_t full = (n >= 64) ? ~0ull : ((1ull << n) - 1);
+  // windows live in the local bits; sharded states keep their top g bits global
+  const int nl = P.nloc;
+  const uint64_t lfull = (nl >= 64) ? ~0ull : ((1ull << nl) - 1);
+  const bool sharded = P.gbits > 0;
   bool gather_all = false;
+  int swapped = 0;
   auto add_unit = [&](uint64_t W, int fwd_pass) {
     LamUnit u;
     u.wmask = W;
+    u.swapped = swapped;
     int l = 0;
     int loc[64];
-    for (int b = 0; b < n; ++b)
+    for (int b = 0; b < nl; ++b)
       if (W >> b & 1) {
         loc[b] = l;
         u.W[l++] = b;
@@ -970,7 +1032,7 @@ std::shared_ptr<Binding> bind(Plan& P, const Pauli& H) {
         KGroup kg{};
         uint32_t xl = 0;
         if (!global)
-          for (int b = 0; b < n; ++b)
+          for (int b = 0; b < nl; ++b)
             if (g.first >> b & 1) xl |= 1u << loc[b];
         kg.xlocal = xl;
         kg.xphys = g.first;
@@ -987,37 +1049,69 @@ std::shared_ptr<Binding> bind(Plan& P, const Pauli& H) {
     left.swap(rest);
     B->units.push_back(u);
   };
-  const PassInfo& last = P.passes.back();
-  add_unit(n <= t ? full : last.wmask, (int)P.passes.size() - 1);
-  while (!left.empty()) {
-    uint64_t W = (1ull << c) - 1;
-    // admit groups in order of fewest extra bits
-    bool grew = true;
-    while (grew) {
-      grew = false;
-      int best = -1, bestc = 1 << 30;
-      for (size_t i = 0; i < left.size(); ++i) {
-        uint64_t nw = W | left[i].first;
-        int cnt = popc64(nw);
-        if ((left[i].first & ~W) == 0 || cnt > t) continue;
-        if (cnt < bestc) {
-          bestc = cnt;
-          best = (int)i;
+  auto greedy_units = [&]() {
+    while (!left.empty()) {
+      uint64_t W = (1ull << c) - 1;
+      bool grew = true;  // admit groups in order of fewest extra bits
+      while (grew) {
+        grew = false;
+        int best = -1, bestc = 1 << 30;
+        for (size_t i = 0; i < left.size(); ++i) {
+          uint64_t nw = W | left[i].first;
+          int cnt = popc64(nw);
+          if ((left[i].first & ~W) == 0 || cnt > t || (left[i].first & ~lfull)) continue;
+          if (cnt < bestc) {
+            bestc = cnt;
+            best = (int)i;
+          }
+        }
+        if (best >= 0) {
+          W |= left[best].first;
+          grew = true;
         }
       }
-      if (best >= 0) {
-        W |= left[best].first;
-        grew = true;
+      for (int b = 0; b < nl && popc64(W) < t; ++b) W |= 1ull << b;
+      size_t before = left.size();
+      add_unit(W, -1);
+      if (left.size() == before) {
+        B->units.pop_back();
+        if (sharded) return;  // partners on another rank: handled after an exchange
+        // flip masks wider than a window: one more unit gathers partners from HBM
+        gather_all = true;
+        add_unit(W, -1);
       }
     }
-    for (int b = 0; b < n && popc64(W) < t; ++b) W |= 1ull << b;
-    size_t before = left.size();
-    add_unit(W, -1);
-    if (left.size() == before) {
-      // flip masks wider than a window: one more unit gathers partners from HBM
-      gather_all = true;
-      B->units.pop_back();
-      add_unit(W, -1);
+  };
+  if (!sharded) {
+    const PassInfo& last = P.passes.back();
+    add_unit(nl <= t ? lfull : last.wmask, (int)P.passes.size() - 1);
+    greedy_units();
+  } else {
+    // groups flipping a global qubit run after the global <-> top-local exchange
+    std::vector<std::pair<uint64_t, std::vector<KPTerm>>> glob, loc0;
+    for (auto& g : left) ((g.first & ~lfull) ? glob : loc0).push_back(g);
+    left = loc0;
+    greedy_units();
+    if (!left.empty()) {
+      B->xmask_ok = false;
+      B->err = "sharded: a Pauli flip mask does not fit one local window";
+      return B;
+    }
+    if (!glob.empty()) {
+      int perm[64];
+      shard_swap_perm(n, P.gbits, perm);
+      for (auto& g : glob) {
+        g.first = remap_mask(g.first, perm, n);
+        for (auto& pt : g.second) pt.zy = remap_mask(pt.zy, perm, n);
+      }
+      left = glob;
+      swapped = 1;
+      greedy_units();
+      if (!left.empty()) {
+        B->xmask_ok = false;
+        B->err = "sharded: a Pauli term flips qubits that are global in both layouts";
+        return B;
+      }
     }
   }
   return B;

@@ -81,6 +81,7 @@ struct GItem {       // finalize items
 };
 
 struct PassInfo {
+  int seg = 0;                      // sharded: segment (layout) this pass runs in
   uint64_t wmask = 0;
   int W[kMaxTileBits + 1] = {0};   // local -> physical bit
   std::vector<int> ops;             // plan op indices in program order
@@ -102,6 +103,7 @@ struct Pauli {
 
 // Lambda evaluation unit: a window pass computing some Pauli groups.
 struct LamUnit {
+  int swapped = 0;      // sharded: computed after the global <-> top-local exchange
   uint64_t wmask = 0;
   int W[kMaxTileBits + 1] = {0};
   int group_begin = 0, group_count = 0;  // into Binding::groups
@@ -131,6 +133,8 @@ struct Plan {
   tcx_dtype dtype = TCX_C64;
   int t = 0, r = 0, c = 0, h = 0;
   int max_ops_per_pass = 0;
+  int gbits = 0, nloc = 0;       // sharded state: global index bits, local bits (= n if not)
+  int nseg = 1;                  // sharded: layouts separated by global<->top-local exchanges
   std::vector<tcx_gate> gates;  // validated input (decode)
   std::vector<double> mats_in;  // input payloads
   std::vector<double> fixed;    // complex (re, im) payloads referenced by ops

@@ -414,7 +414,8 @@ tcx_status jit_prepare(Plan& P, int kind, bool mega, const Binding* Bd) {
       if (kind == 1) keys.push_back(jit_key_pass(p, 1));
     }
     if (Bd)
-      for (int u = 1; u < (int)Bd->units.size(); ++u) keys.push_back(jit_key_lambda(Bd->hash, u));
+      for (int u = P.gbits > 0 ? 0 : 1; u < (int)Bd->units.size(); ++u)
+        keys.push_back(jit_key_lambda(Bd->hash, u));
   }
   std::string err;
   if (!jit_build(P, keys, err)) return fail(TCX_E_CUDA, err);
@@ -479,10 +480,10 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 WsLayout ws_layout(const Plan& P, const Binding* Bd, int64_t B, int kind, bool host_io) {
   WsLayout w{};
   const size_t rs = P.dtype == TCX_C128 ? 8 : 4;
-  const size_t N = size_t(1) << P.n;
+  const size_t N = size_t(1) << P.nloc;  // this rank's amplitudes (= 2^n unless sharded)
   const int64_t S = P.tiles / tiles_per_cta(P);
   const int EU = Bd ? (int)Bd->units.size() : 1;
-  w.mega = kind != K_STATE && P.passes.size() == 1 && EU == 1;
+  w.mega = kind != K_STATE && P.passes.size() == 1 && EU == 1 && P.gbits == 0;
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
@@ -532,9 +533,19 @@ double lambda_flops(const Binding& B, const LamUnit& u) {
   return f;
 }
 
+// one step of a sharded program (tcx_shard_exec); nullptr = the whole single-GPU program
+struct OneStep {
+  int kind, arg, rank;
+  bool first_lambda;
+};
+
 tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, double* E,
                double* grad, void* state, void* ws, size_t ws_bytes, cudaStream_t st, int kind,
-               const WsLayout* wl_in) {
+               const WsLayout* wl_in, const OneStep* one = nullptr) {
+  if (P.gbits > 0 && !one)
+    return fail(TCX_E_INVALID, "sharded circuit (global_bits > 0): use tcx_shard_program/exec");
+  auto want = [&](int k, int a) { return !one || (one->kind == k && one->arg == a); };
+  const uint64_t gbase = one ? ((uint64_t)one->rank << P.nloc) : 0ull;
   if (B <= 0) return fail(TCX_E_INVALID, "B must be > 0");
   if (!ws) return fail(TCX_E_INVALID, "null workspace");
   if (P.P > 0 && !theta) return fail(TCX_E_INVALID, "null theta");
@@ -568,7 +579,7 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
   const int EU = Bd ? (int)Bd->units.size() : 1;
   const int64_t kMaxRows = 65535;
   // ---- materialize per-theta matrices
-  for (int64_t b0 = 0; b0 < B; b0 += kMaxRows) {
+  for (int64_t b0 = 0; b0 < B && want(0, 0); b0 += kMaxRows) {
     const int64_t rows = std::min(kMaxRows, B - b0);
     if (P.mitems.empty()) break;
     MatArgs ma;
@@ -603,7 +614,7 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
     a.swb = (const uint32_t*)DT->swb.p;
     a.wmask = wmask;
     for (int l = 0; l < P.t; ++l) a.W[l] = Wl[l];
-    a.n = P.n;
+    a.n = P.nloc;
     a.t = P.t;
     a.h = P.h;
     a.mat_total = P.mat_total;
@@ -651,10 +662,10 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
         Drv& D = drv();
         const int ns = P.jit_nsub;
         if (b0 == 0) {
-          const TmaDims td = tma_dims(P.n, a.wmask, c128);
+          const TmaDims td = tma_dims(P.nloc, a.wmask, c128);
           a.use_tma = 0;
-          if (td.rank > 0 && ns == 1 && encode_tmap(a.tmap[0], a.psi, td, P.n, B))
-            a.use_tma = (wl.lam == 0 || encode_tmap(a.tmap[1], a.lam, td, P.n, B)) ? 1 : 0;
+          if (td.rank > 0 && ns == 1 && encode_tmap(a.tmap[0], a.psi, td, P.nloc, B))
+            a.use_tma = (wl.lam == 0 || encode_tmap(a.tmap[1], a.lam, td, P.nloc, B)) ? 1 : 0;
           if (!(a.mode & (M_LOAD_PSI | M_LOAD_LAM | M_STORE_PSI | M_STORE_LAM))) a.use_tma = 0;
         }
         const SmemLayout LJ = smem_layout(a.t, a.h, rs, a.mat_count, a.max_stage_acc,
@@ -686,7 +697,7 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
     }
     return TCX_OK;
   };
-  const double Nf = (double)((int64_t)1 << P.n), csz = 2.0 * rs, Bf = (double)B;
+  const double Nf = (double)((int64_t)1 << P.nloc), csz = 2.0 * rs, Bf = (double)B;
   auto launch = [&](PassArgs& a, int phase, int index, double flops_amp) -> tcx_status {
     std::string jkey;
     if (P.jit_on) {
@@ -731,13 +742,16 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
                       (kind == K_GRAD ? pass_flops(P, p, true) : 0.0);
     if ((s = launch(a, 5, 0, fl))) return s;
   } else {
+    const bool sharded = P.gbits > 0;
     for (int pi = 0; pi < nP; ++pi) {
+      if (!want(1, pi)) continue;
       const PassInfo& p = P.passes[pi];
-      const bool last = pi == nP - 1;
+      const bool last = pi == nP - 1 && !sharded;  // sharded: every lambda unit is its own step
       int mode = M_FWD | M_STORE_PSI | (pi == 0 ? M_INIT : M_LOAD_PSI);
       PassArgs a;
       base_args(a, p.wmask, p.W, mode);
       set_pass(a, p, true);
+      a.gbase = gbase;
       if (last && kind != K_STATE) {
         a.mode |= M_LAMBDA | (kind == K_GRAD ? M_STORE_LAM : 0);
         if (kind != K_GRAD && EU == 1) a.mode &= ~M_STORE_PSI;
@@ -750,11 +764,15 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
       if ((s = launch(a, 1, pi, fl))) return s;
     }
     if (kind != K_STATE) {
-      for (int u = 1; u < EU; ++u) {
+      for (int u = sharded ? 0 : 1; u < EU; ++u) {
+        if (!want(2, u)) continue;
         const LamUnit& U = Bd->units[u];
         PassArgs a;
-        int mode = M_LOAD_PSI | M_LAMBDA | (kind == K_GRAD ? (M_LOAD_LAM | M_STORE_LAM) : 0);
+        const bool load_lam = sharded ? !one->first_lambda : true;
+        int mode = M_LOAD_PSI | M_LAMBDA |
+                   (kind == K_GRAD ? ((load_lam ? M_LOAD_LAM : 0) | M_STORE_LAM) : 0);
         base_args(a, U.wmask, U.W, mode);
+        a.gbase = gbase;
         a.nstages = 0;
         a.mat_count = 0;
         a.acc_count = 0;
@@ -766,18 +784,20 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
     }
     if (kind == K_GRAD) {
       for (int pi = nP - 1; pi >= 0; --pi) {
+        if (!want(3, pi)) continue;
         const PassInfo& p = P.passes[pi];
         int mode = M_LOAD_PSI | M_LOAD_LAM | M_BWD | (pi > 0 ? (M_STORE_PSI | M_STORE_LAM) : 0);
         PassArgs a;
         base_args(a, p.wmask, p.W, mode);
         set_pass(a, p, true);
+        a.gbase = gbase;
         if ((s = launch(a, 3, pi, pass_flops(P, p, true)))) return s;
       }
     }
   }
   // ---- finalize / export
   if (kind != K_STATE) {
-    for (int64_t b0 = 0; b0 < B; b0 += kMaxRows) {
+    for (int64_t b0 = 0; b0 < B && want(4, 0); b0 += kMaxRows) {
       const int64_t rows = std::min(kMaxRows, B - b0);
       FinArgs f;
       f.part = (const double*)(W + wl.part);
@@ -802,7 +822,7 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
       finalize_kernel<<<(unsigned)rows, 256, 0, st>>>(f);
       CUDA_TRY(cudaGetLastError());
     }
-  } else {
+  } else if (!one) {
     const size_t bytes = (size_t)B * ((size_t)1 << P.n) * 2 * rs;
     if (!P.relabeled) {
       CUDA_TRY(cudaMemcpyAsync(state, W + wl.psi, bytes, cudaMemcpyDeviceToDevice, st));
@@ -1009,6 +1029,8 @@ tcx_status tcx_circuit_info(const tcx_circuit* circ, const tcx_pauli* pauli, tcx
   o->unitary = P.unitary;
   o->relabeled = P.relabeled;
   o->jit = P.jit_on ? 1 : 0;
+  o->global_bits = P.gbits;
+  o->segments = P.nseg;
   o->tiles_per_state = P.tiles;
   o->acc_slots = P.acc_total;
   o->mat_reals = P.mat_total;
@@ -1050,6 +1072,91 @@ tcx_status tcx_profile_read(tcx_kernel_time* out, int32_t cap, int32_t* n) {
   }
   g_prof.log.clear();
   *n = std::min(k, cap);
+  return TCX_OK;
+}
+
+tcx_status tcx_shard_program(const tcx_circuit* circ, const tcx_pauli* pauli, int32_t want_grad,
+                             tcx_shard_step* steps, int32_t cap, int32_t* n) {
+  g_err.clear();
+  if (!circ || !pauli || !n) return fail(TCX_E_INVALID, "null argument");
+  Plan& P = const_cast<tcx_circuit*>(circ)->plan;
+  std::shared_ptr<Binding> Bd;
+  tcx_status s = binding_for(P, pauli, Bd, nullptr);
+  if (s) return s;
+  std::vector<tcx_shard_step> v;
+  auto add = [&](int k, int a) { v.push_back({k, a}); };
+  const int nP = (int)P.passes.size();
+  add(TCX_STEP_MATERIALIZE, 0);
+  for (int p = 0; p < nP; ++p) {
+    if (p > 0 && P.passes[p].seg != P.passes[p - 1].seg) add(TCX_STEP_EXCHANGE, 1);
+    add(TCX_STEP_FWD, p);
+  }
+  const int x = want_grad ? 3 : 1;  // exchange psi (+ lambda once it exists)
+  bool any_lam = false;
+  for (int u = 0; u < (int)Bd->units.size(); ++u)
+    if (!Bd->units[u].swapped) {
+      add(TCX_STEP_LAMBDA, u);
+      any_lam = true;
+    }
+  bool sw = false;
+  for (int u = 0; u < (int)Bd->units.size(); ++u)
+    if (Bd->units[u].swapped) {
+      if (!sw) add(TCX_STEP_EXCHANGE, any_lam ? x : 1);
+      sw = true;
+      add(TCX_STEP_LAMBDA, u);
+    }
+  if (sw) add(TCX_STEP_EXCHANGE, x);
+  if (want_grad)
+    for (int p = nP - 1; p >= 0; --p) {
+      add(TCX_STEP_BWD, p);
+      if (p > 0 && P.passes[p].seg != P.passes[p - 1].seg) add(TCX_STEP_EXCHANGE, 3);
+    }
+  add(TCX_STEP_FINALIZE, 0);
+  *n = (int32_t)v.size();
+  if (steps)
+    for (int i = 0; i < std::min<int>(cap, (int)v.size()); ++i) steps[i] = v[i];
+  return TCX_OK;
+}
+
+tcx_status tcx_shard_exec(const tcx_circuit* circ, const tcx_pauli* pauli, int32_t rank,
+                          int32_t want_grad, const tcx_shard_step* step, const double* theta,
+                          int64_t B, double* E_partial, double* grad_partial, void* ws,
+                          size_t ws_bytes, void* stream) {
+  g_err.clear();
+  if (!circ || !step) return fail(TCX_E_INVALID, "null argument");
+  Plan& P = const_cast<tcx_circuit*>(circ)->plan;
+  if (P.gbits == 0) return fail(TCX_E_INVALID, "circuit is not sharded (global_bits = 0)");
+  if (rank < 0 || rank >= (1 << P.gbits)) return fail(TCX_E_INVALID, "rank out of range");
+  if (step->kind == TCX_STEP_EXCHANGE) return fail(TCX_E_INVALID, "exchange steps run in the caller");
+  OneStep one{step->kind, step->arg, rank, false};
+  if (step->kind == TCX_STEP_LAMBDA) {  // the first lambda unit initialises lambda
+    std::shared_ptr<Binding> Bd;
+    if (!pauli) return fail(TCX_E_INVALID, "null pauli");
+    tcx_status s = binding_for(P, pauli, Bd, nullptr);
+    if (s) return s;
+    int first = -1;
+    for (int u = 0; u < (int)Bd->units.size() && first < 0; ++u)
+      if (!Bd->units[u].swapped) first = u;
+    if (first < 0) first = 0;
+    one.first_lambda = step->arg == first;
+  }
+  return run(P, pauli, theta, B, E_partial, grad_partial, nullptr, ws, ws_bytes,
+             (cudaStream_t)stream, want_grad ? K_GRAD : K_EXPECT, nullptr, &one);
+}
+
+tcx_status tcx_shard_buffers(const tcx_circuit* circ, const tcx_pauli* pauli, int64_t B,
+                             int32_t want_grad, void* ws, void** psi, void** lam,
+                             int64_t* local_amps) {
+  g_err.clear();
+  if (!circ || !pauli || !psi || !lam || !local_amps) return fail(TCX_E_INVALID, "null argument");
+  Plan& P = const_cast<tcx_circuit*>(circ)->plan;
+  std::shared_ptr<Binding> Bd;
+  tcx_status s = binding_for(P, pauli, Bd, nullptr);
+  if (s) return s;
+  WsLayout wl = ws_layout(P, Bd.get(), B, want_grad ? K_GRAD : K_EXPECT, false);
+  *psi = (char*)ws + wl.psi;
+  *lam = want_grad ? (char*)ws + wl.lam : nullptr;
+  *local_amps = (int64_t)1 << P.nloc;
   return TCX_OK;
 }
 

@@ -44,14 +44,15 @@ class tcx_gate(ctypes.Structure):
 class tcx_build_opts(ctypes.Structure):
     _fields_ = [("tile_bits", ctypes.c_int32), ("reg_bits", ctypes.c_int32),
                 ("coalesce_bits", ctypes.c_int32), ("max_ops_per_pass", ctypes.c_int32),
-                ("jit", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
+                ("jit", ctypes.c_int32), ("global_bits", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 2)]
 
 
 class tcx_plan_info(ctypes.Structure):
     _fields_ = [(f, ctypes.c_int32) for f in (
         "n_qubits", "n_params", "dtype", "tile_bits", "reg_bits", "coalesce_bits",
         "threads_per_tile", "n_ops", "fwd_passes", "lambda_passes", "bwd_passes", "stages",
-        "unitary", "relabeled", "jit")] + [(f, ctypes.c_int64) for f in (
+        "unitary", "relabeled", "jit", "global_bits", "segments")] + [(f, ctypes.c_int64) for f in (
             "tiles_per_state", "acc_slots", "mat_reals")]
 
     def as_dict(self):
@@ -64,6 +65,13 @@ class tcx_kernel_time(ctypes.Structure):
 
 
 PHASES = {0: "materialize", 1: "forward", 2: "lambda", 3: "backward", 4: "finalize", 5: "fused"}
+
+
+class tcx_shard_step(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("arg", ctypes.c_int32)]
+
+
+STEP_MATERIALIZE, STEP_FWD, STEP_LAMBDA, STEP_BWD, STEP_FINALIZE, STEP_EXCHANGE = range(6)
 
 _vp, _i32, _i64, _sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -83,6 +91,11 @@ _sig = {
     "tcx_launch_count": [_vp, _vp, _i64, _i32, ctypes.POINTER(_i32)],
     "tcx_profile_enable": [_i32],
     "tcx_circuit_jit": [_vp, _vp, _i64, _i32],
+    "tcx_shard_program": [_vp, _vp, _i32, ctypes.POINTER(tcx_shard_step), _i32, ctypes.POINTER(_i32)],
+    "tcx_shard_exec": [_vp, _vp, _i32, _i32, ctypes.POINTER(tcx_shard_step), _vp, _i64, _vp, _vp,
+                       _vp, _sz, _vp],
+    "tcx_shard_buffers": [_vp, _vp, _i64, _i32, _vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                          ctypes.POINTER(_i64)],
     "tcx_profile_read": [ctypes.POINTER(tcx_kernel_time), _i32, ctypes.POINTER(_i32)],
 }
 for _name, _args in _sig.items():
@@ -130,7 +143,7 @@ class Circuit:
 
     def __init__(self, circ, dtype: str = "c64", tile_bits: int = 0, reg_bits: int = 0,
                  coalesce_bits: int = 0, max_ops_per_pass: int = 0, jit: bool = True,
-                 gates=None):
+                 global_bits: int = 0, gates=None):
         names, q0, q1, param, coeff, moff, mats = circ.arrays()
         self.n = circ.n
         self.P = circ.n_params
@@ -142,7 +155,8 @@ class Circuit:
             mats = np.zeros(2)
         self._mats = mats
         opts = tcx_build_opts(tile_bits, reg_bits, coalesce_bits, max_ops_per_pass,
-                              0 if jit else -1)
+                              0 if jit else -1, global_bits)
+        self.global_bits = global_bits
         h = _vp()
         _check(_lib.tcx_circuit_build(self.n, self.P, self._gates, self.G,
                                       mats.ctypes.data_as(_dp), mats.size // 2,
