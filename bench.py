@@ -146,6 +146,8 @@ def main():
     ap.add_argument("--impl", default="tcx", choices=["tcx", "reference"])
     ap.add_argument("--config", type=int, default=1, help="BASELINE.json configs index")
     ap.add_argument("--batch", type=int, default=None, help="theta rows per rank")
+    ap.add_argument("--batch-qubits", type=int, default=None,
+                    help="config 4: local qubits per rank (default 33)")
     ap.add_argument("--tile-bits", type=int, default=0)
     ap.add_argument("--max-ops-per-pass", type=int, default=0)
     ap.add_argument("--jit", type=int, default=1, help="1: per-circuit specialised kernels")
@@ -153,6 +155,8 @@ def main():
                     help="grad (E + adjoint gradient, default) or expect (forward + E only; cfg4)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-rows", type=int, default=8)
+    ap.add_argument("--virtual-ranks", type=int, default=1,
+                    help="config 4 on one GPU: shard the state over this many virtual ranks")
     ap.add_argument("--cpu-rows", type=int, default=8)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "tcx" else args.warmup
@@ -172,6 +176,9 @@ def main():
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=dev)
+
+    if args.config == 4 and (world > 1 or args.virtual_ranks > 1):
+        return run_sharded(args, world, rank, local, dev)
 
     name, circ, H, theta, dtype = W.config(args.config, B=args.batch)
     B = theta.shape[0]
@@ -333,6 +340,83 @@ def main():
                 "d2h_bytes_per_step": int(B * 8 + (B * circ.n_params * 8 if mode == "grad" else 0))},
         "gpu_launches": int(launches),
         "clocks": clk,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def run_sharded(args, world, rank, local, dev):
+    """configs[4]: one (33 + log2 G)-qubit complex64 state sharded over G ranks on its top
+    log2 G qubits (weak scaling), NCCL all-to-all qubit exchanges, TFIM <H> + adjoint grad."""
+    import torch
+    import torch.distributed as dist
+    from paper_2205_10091_b200 import tcx
+    from paper_2205_10091_b200.shard import ShardedState
+    G = world if world > 1 else args.virtual_ranks
+    g = G.bit_length() - 1
+    assert 1 << g == G, "G must be a power of two"
+    n = (args.batch_qubits or (33 if world > 1 else 30 - g)) + g
+    name, circ, H, theta, dtype = W.config(4, n=n)
+    grp = dist.group.WORLD if world > 1 else None
+    S = ShardedState(circ, H, dtype, g, ranks=[rank] if world > 1 else None, dist_group=grp,
+                     jit=bool(args.jit), device=dev)
+    t0 = time.perf_counter()
+    S.C.compile(S.Pl, B=1, kind="grad")
+    t_jit = time.perf_counter() - t0
+    th = torch.as_tensor(theta).to(dev)
+    for _ in range(args.warmup):
+        S.run(th)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(local)
+    clocks.start()
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tcx.profile_enable(True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        E, Gr = S.run(th)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    tcx.profile_enable(False)
+    prof = tcx.profile_read()
+    clk = clocks.stop()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    kms = sum(p[2] for p in prof)
+    # e2e: theta from pinned host memory in, E / grad back, every step
+    th_h = torch.as_tensor(theta).pin_memory()
+    t1 = time.perf_counter()
+    for _ in range(args.steps):
+        E, Gr = S.run(th_h.to(dev, non_blocking=True))
+        E.cpu(), Gr.cpu()
+    e2e_s = time.perf_counter() - t1
+    info = S.C.info(S.Pl)
+    line = {
+        "metric": "sharded single-state <H>+grad circuits/s (%s)" % name,
+        "value": args.steps / (ms / 1e3), "unit": "circuits/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c64",
+        "data": "synthetic",
+        "config": {"workload": name, "n_qubits": n, "global_bits": g, "ranks": G,
+                   "virtual_ranks": world == 1, "plan": {k: info[k] for k in (
+                       "fwd_passes", "segments", "lambda_passes", "jit")},
+                   "jit_compile_s": round(t_jit, 2),
+                   "l2": "inputs larger than L2 (2^%d amplitudes per rank)" % (n - g)},
+        "kernel_ms_per_step": kms / args.steps,
+        "exchange_and_other_ms_per_step": (ms - kms) / args.steps,
+        "e2e": {"value": args.steps / e2e_s, "unit": "circuits/s", "h2d_bytes_per_step": int(theta.size * 8),
+                "d2h_bytes_per_step": int(8 + theta.size * 8)},
+        "gpu_launches": len(prof) // max(args.steps, 1) * args.steps,
+        "clocks": clk, "cpu_baseline": None,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

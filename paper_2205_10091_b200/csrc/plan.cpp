@@ -168,6 +168,37 @@ void normalize_diag(Op& op) {
   op.has_param = !par.empty();
 }
 
+// Structured 2x2 class of a fused 1-qubit run (KOp.nterm of a U1 op; the JIT skips the
+// identically-zero coefficients and, in the adjoint, the R' entries the generator never
+// reads).  Each class is closed under products:
+//   1 XT  [[re, i re], [i re, re]]: I, Z, Y, RX      generator X -> B = +-X (R'01, R'10)
+//   2 RE  real:                     I, Z, X, H, RY   generator Y -> B = det(S) Y (R'01, R'10)
+//   3 DG  diagonal:                 I, Z, S, T, RZ   generator Z -> B = Z (R'00, R'11)
+// 0 = general (any TCX_U1 payload or mixed classes).  TCX_U1_STRUCT=0 disables.
+int u1_class(const std::vector<Constituent>& cons) {
+  static const int off = [] {
+    const char* e = std::getenv("TCX_U1_STRUCT");
+    return e && e[0] == '0';
+  }();
+  if (off) return 0;
+  unsigned m = 7;  // bit k-1: class k possible
+  for (const auto& c : cons) {
+    unsigned k = 0;
+    switch (c.kind) {
+      case TCX_I: case TCX_Z: k = 7; break;
+      case TCX_RX: case TCX_Y: k = 1; break;
+      case TCX_RY: case TCX_X: case TCX_H: k = 2; break;
+      case TCX_RZ: case TCX_S: case TCX_SDG: case TCX_T: case TCX_TDG: k = 4; break;
+      default: k = 0; break;
+    }
+    m &= k;
+  }
+  if (m & 4) return 3;
+  if (m & 2) return 2;
+  if (m & 1) return 1;
+  return 0;
+}
+
 // ------------------------------------------------------------- scheduling
 double op_weight(const Op& o) {
   switch (o.type) {
@@ -838,6 +869,7 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
         ko.mat = (int16_t)(mat - pass.mat_begin);
         if (o.type == OP_U1) {
           ko.a = (uint8_t)slot_of(o.b0);
+          ko.nterm = (int16_t)u1_class(o.cons);
         } else if (o.type == OP_U2F) {  // tile-local positions (shared-memory op)
           ko.a = (uint8_t)loc[o.b0];
           ko.b = (uint8_t)loc[o.b1];

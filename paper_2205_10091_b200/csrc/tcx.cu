@@ -873,7 +873,7 @@ tcx_status tcx_circuit_build(int32_t n_qubits, int32_t n_params, const tcx_gate*
     const Plan& P = c->plan;
     if (!jit_available(&why)) {
       c->plan.jit_note = why;
-    } else if (P.passes.size() > 48 || P.ops.size() > 4096) {
+    } else if (P.passes.size() > 512 || P.ops.size() > 32768) {
       c->plan.jit_note = "circuit too large for per-pass specialisation";
     } else {
       c->plan.jit_on = true;  // kernels are generated and compiled on first use

@@ -137,6 +137,41 @@ def test_grad_hea_heisenberg_multi_tile(tc, dtype, jit):
     check_grad(G, Gr, H, c, dtype)
 
 
+def _structured_circuit(n, seed):
+    """Fused 1-qubit runs of every structured class (plan.cpp u1_class): XT (RX, Y, Z),
+    RE (RY, X, H, Z), DG (RZ, S, T next to a non-diagonal breaks into DIAG), general."""
+    rng = np.random.default_rng(seed)
+    runs = [["h", "ry"], ["x", "ry", "z"], ["ry", "h", "ry"], ["y", "rx"], ["rx", "z", "rx"],
+            ["rx"], ["ry"], ["rx", "ry"], ["z", "rx", "y"], ["h", "rx"]]
+    c = W.Circuit(n, 6)
+    for layer in range(4):
+        for q in range(n):
+            for k in runs[int(rng.integers(len(runs)))]:
+                if k in ("rx", "ry"):
+                    c.add(k, q, param=int(rng.integers(6)), coeff=float(rng.uniform(-2, 2)))
+                else:
+                    c.add(k, q)
+        for q in range(layer % 2, n - 1, 2):
+            c.add("cnot", q, q + 1)
+    return c
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("n,t", [(6, None), (13, 8)])
+def test_grad_structured_u1_classes(tc, dtype, n, t):
+    """Structured-class U1 kernels (zero coefficients and unused R' entries skipped) vs the
+    oracle; the interpreter (jit=False) runs the general form of the same ops."""
+    c = _structured_circuit(n, 11 + n)
+    H = W.random_pauli_sum(n, 10, n)
+    th = W.thetas(3, 6, n)
+    opts = {} if t is None else {"tile_bits": t, "coalesce_bits": 2}
+    E, G, C = run_grad(tc, c, H, th, dtype, jit=True, **opts)
+    assert C.info()["jit"] == 1
+    Er, Gr = oracle_grad(c, H, th)
+    check_E(E, Er, H, dtype)
+    check_grad(G, Gr, H, c, dtype)
+
+
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
 def test_expect_matches_grad_E(tc, dtype):
     c, H = W.hea(12, 3), W.tfim_zz_x(12)
