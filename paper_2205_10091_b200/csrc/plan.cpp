@@ -175,7 +175,7 @@ void normalize_diag(Op& op) {
 //   2 RE  real:                     I, Z, X, H, RY   generator Y -> B = det(S) Y (R'01, R'10)
 //   3 DG  diagonal:                 I, Z, S, T, RZ   generator Z -> B = Z (R'00, R'11)
 // 0 = general (any TCX_U1 payload or mixed classes).  TCX_U1_STRUCT=0 disables.
-int u1_class(const std::vector<Constituent>& cons) {
+int u1_class_of(const std::vector<Constituent>& cons) {
   static const int off = [] {
     const char* e = std::getenv("TCX_U1_STRUCT");
     return e && e[0] == '0';
@@ -463,6 +463,8 @@ void thread_order(uint32_t Rloc, int t, bool c128, int8_t* T) {
 }
 
 }  // namespace
+
+int u1_class(const std::vector<Constituent>& cons) { return u1_class_of(cons); }
 
 // Swizzle of the tile-local element index in shared memory: the low lg bits (bank
 // group within a 128-byte row) are XORed with a GF(2)-linear image of the higher bits,
@@ -869,7 +871,7 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
         ko.mat = (int16_t)(mat - pass.mat_begin);
         if (o.type == OP_U1) {
           ko.a = (uint8_t)slot_of(o.b0);
-          ko.nterm = (int16_t)u1_class(o.cons);
+          ko.nterm = (int16_t)u1_class_of(o.cons);
         } else if (o.type == OP_U2F) {  // tile-local positions (shared-memory op)
           ko.a = (uint8_t)loc[o.b0];
           ko.b = (uint8_t)loc[o.b1];

@@ -180,6 +180,7 @@ struct TmaDims {
 TmaDims tma_dims(int n, uint64_t wmask, bool c128);
 
 // Build; returns TCX_OK or an error with message.
+int u1_class(const std::vector<Constituent>& cons);  // plan.cpp: 0 general, 1 XT, 2 RE, 3 DG
 tcx_status build_plan(int n, int P, const tcx_gate* gates, int64_t G, const double* mats,
                       int64_t nmat, tcx_dtype dtype, const tcx_build_opts* opts, Plan& plan,
                       std::string& err);

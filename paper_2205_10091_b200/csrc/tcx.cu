@@ -509,13 +509,16 @@ WsLayout ws_layout(const Plan& P, const Binding* Bd, int64_t B, int kind, bool h
 }
 
 // ---- algorithmic cost model: real flops per amplitude, complex
-// multiply = 6, complex add = 2.
+// multiply = 6, complex add = 2, real x complex = 2.
 double op_flops(const Op& o, bool bwd) {
   const double nt = (double)o.terms.size();
   double npar = 0;
   for (auto& t : o.terms) npar += t.param >= 0;
   switch (o.type) {
-    case OP_U1: return bwd ? 28.0 + (o.has_param ? 16.0 : 0.0) : 14.0;
+    case OP_U1:
+      if (u1_class(o.cons))  // structured: real scalar x complex terms, half the R' entries
+        return bwd ? 12.0 + (o.has_param ? 8.0 : 0.0) : 6.0;
+      return bwd ? 28.0 + (o.has_param ? 16.0 : 0.0) : 14.0;
     case OP_U2F: return bwd ? 60.0 : 30.0;
     case OP_CX: return 0.0;
     default: return bwd ? 12.0 * nt + 2.0 * npar : 6.0 * nt;
