@@ -19,7 +19,7 @@ namespace dev {
 
 // ---- the window pass kernel --------------------------------------------------
 template <typename Real, int RB, int KM>
-__global__ void __launch_bounds__(256, 2) pass_kernel(const PassArgs a) {
+__global__ void __launch_bounds__(512, 1) pass_kernel(const PassArgs a) {
   using C = Cx<Real>;
   constexpr int NR = 1 << RB;
   constexpr bool kFwd = KM == KM_FWD || KM == KM_MEGA;

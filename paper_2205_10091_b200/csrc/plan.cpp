@@ -650,9 +650,9 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
   int r = opts && opts->reg_bits > 0 ? opts->reg_bits : (t < tdef ? 3 : 4);
   r = std::min(r, kMaxRegBits);
   if (r > t) r = t;
-  if (t - r > 8) r = t - 8;  // at most 256 threads per tile (kernel launch bounds)
+  if (t - r > 9) r = t - 9;  // at most 512 threads per tile (kernel launch bounds)
   if (r > kMaxRegBits) {
-    err = "tile_bits too large: needs reg_bits <= 4 with <= 256 threads (t <= 12)";
+    err = "tile_bits too large: needs reg_bits <= 4 with <= 512 threads (t <= 13)";
     return TCX_E_INVALID;
   }
   if (c > t) c = t;

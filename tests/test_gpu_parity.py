@@ -172,6 +172,32 @@ def test_grad_structured_u1_classes(tc, dtype, n, t):
     check_grad(G, Gr, H, c, dtype)
 
 
+@pytest.mark.parametrize("jit", [True, False])
+@pytest.mark.parametrize("n", [13, 16])
+def test_grad_512_thread_tiles(tc, n, jit):
+    """t = 13 (2^13-amplitude tiles, 512 threads per CTA) for complex64 E + grad."""
+    c, H = W.hea(n, 3), W.heisenberg(n)
+    th = W.thetas(2, c.n_params, 9)
+    E, G, C = run_grad(tc, c, H, th, "c64", tile_bits=13, jit=jit)
+    assert C.info()["threads_per_tile"] == 512
+    Er, Gr = oracle_grad(c, H, th)
+    check_E(E, Er, H, "c64")
+    check_grad(G, Gr, H, c, "c64")
+
+
+@pytest.mark.parametrize("jit", [True, False])
+def test_expect_512_thread_tiles_c128(tc, jit):
+    """complex128 forward-only with 2^13-amplitude tiles (128 KB of shared memory)."""
+    n = 15
+    c = W.random_deep_circuit(n, 12, 5)
+    H = W.pauli_sum(n, [({0: "Z"}, 1.0), ({3: "X", 4: "X"}, 0.5)])
+    C, P = tc.Circuit(c, "c128", tile_bits=13, jit=jit), tc.Pauli(H)
+    assert C.info()["threads_per_tile"] == 512
+    E = tc.expect_batch(C, P, _th(np.zeros((1, 0)))).cpu().numpy()
+    Er = orc.expect_batch(c, H, np.zeros((1, 0)))
+    check_E(E, Er, H, "c128")
+
+
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
 def test_expect_matches_grad_E(tc, dtype):
     c, H = W.hea(12, 3), W.tfim_zz_x(12)
