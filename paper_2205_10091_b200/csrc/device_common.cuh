@@ -133,6 +133,7 @@ __device__ __forceinline__ float qy(q64 v) {
   return b;
 }
 __device__ __forceinline__ q64 qsw(q64 v) { return qpk(qy(v), qx(v)); }
+__device__ __forceinline__ q64 qneg(q64 v) { return qpk(-qx(v), -qy(v)); }
 __device__ __forceinline__ q64 qfma(q64 a, q64 b, q64 c) {  // a * b + c, per half
   q64 d;
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
@@ -261,22 +262,19 @@ __device__ __forceinline__ void apply_u1_dag(Cx<Real>* v, const Real (&m)[8]) {
     v[j1].y = m[2] * p.y - m[3] * p.x + m[6] * q.y - m[7] * q.x;
   }
 }
-// R'_ab += psi_a conj(lambda_b) over the pairs of slot K (a, b = value of the bit).
+// Pauli components of R' (R'_ab = sum psi_a conj(lambda_b) over the pairs of slot K):
+// c[0] = Im(R'01 + R'10), c[1] = Re(R'01 - R'10), c[2] = Im(R'00 - R'11), so that
+// Im Tr(B R') = bx c0 + by c1 + bz c2 for B = bx X + by Y + bz Z (finalize_kernel).
 template <int RB, int K, typename Real>
-__device__ __forceinline__ void accum_r(const Cx<Real>* v, const Cx<Real>* l, Real (&r)[8]) {
+__device__ __forceinline__ void accum_c3(const Cx<Real>* v, const Cx<Real>* l, Real (&c)[3]) {
 #pragma unroll
   for (int j = 0; j < (1 << RB); ++j) {
     if (j & (1 << K)) continue;
     const int j1 = j | (1 << K);
     const Cx<Real> p0 = v[j], p1 = v[j1], l0 = l[j], l1 = l[j1];
-    r[0] = fma(p0.x, l0.x, fma(p0.y, l0.y, r[0]));
-    r[1] = fma(p0.y, l0.x, fma(-p0.x, l0.y, r[1]));
-    r[2] = fma(p0.x, l1.x, fma(p0.y, l1.y, r[2]));
-    r[3] = fma(p0.y, l1.x, fma(-p0.x, l1.y, r[3]));
-    r[4] = fma(p1.x, l0.x, fma(p1.y, l0.y, r[4]));
-    r[5] = fma(p1.y, l0.x, fma(-p1.x, l0.y, r[5]));
-    r[6] = fma(p1.x, l1.x, fma(p1.y, l1.y, r[6]));
-    r[7] = fma(p1.y, l1.x, fma(-p1.x, l1.y, r[7]));
+    c[0] = fma(p0.y, l1.x, fma(-p0.x, l1.y, fma(p1.y, l0.x, fma(-p1.x, l0.y, c[0]))));
+    c[1] = fma(p0.x, l1.x, fma(p0.y, l1.y, fma(-p1.x, l0.x, fma(-p1.y, l0.y, c[1]))));
+    c[2] = fma(p0.y, l0.x, fma(-p0.x, l0.y, fma(-p1.y, l1.x, fma(p1.x, l1.y, c[2]))));
   }
 }
 // CNOT with target slot KT and control register slot KC: register swaps.
@@ -343,41 +341,38 @@ __device__ __forceinline__ Real warp_sum(Real x, int width) {
   for (int o = (width >= 32 ? 16 : width >> 1); o > 0; o >>= 1) x += __shfl_xor_sync(mask, x, o);
   return x;
 }
-// Transposed butterfly: 8 values over 32 lanes in 9 shuffles; lane (l & 3) == 0 ends
-// with value index 4*b4 + 2*b3 + b2 and writes it to dst[index].
+// Transposed butterfly for 3 values in 6 shuffles; lanes 0 / 16 / 8 end with the sums of
+// r[0] / r[1] / r[2] and write dst[0..2].
 template <typename Real>
-__device__ __forceinline__ void warp_sum8(Real (&r)[8], int lane, int width, Real* dst) {
+__device__ __forceinline__ void warp_sum3(Real (&r)[3], int lane, int width, Real* dst) {
   if (width >= 32) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const bool hi = lane & 16;
-      const Real send = hi ? r[k] : r[k + 4];
-      const Real keep = hi ? r[k + 4] : r[k];
-      r[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const bool hi = lane & 8;
-      const Real send = hi ? r[k] : r[k + 2];
-      const Real keep = hi ? r[k + 2] : r[k];
-      r[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
-    {
-      const bool hi = lane & 4;
-      const Real send = hi ? r[0] : r[1];
-      const Real keep = hi ? r[1] : r[0];
-      r[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    }
-    r[0] += __shfl_xor_sync(0xffffffffu, r[0], 2);
-    r[0] += __shfl_xor_sync(0xffffffffu, r[0], 1);
-    if ((lane & 3) == 0) dst[((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1)] = r[0];
+    const bool h16 = lane & 16, h8 = lane & 8;
+    const Real u = (h16 ? r[1] : r[0]) + __shfl_xor_sync(0xffffffffu, h16 ? r[0] : r[1], 16);
+    const Real z = r[2] + __shfl_xor_sync(0xffffffffu, r[2], 16);
+    Real w = (h8 ? z : u) + __shfl_xor_sync(0xffffffffu, h8 ? u : z, 8);
+    w += __shfl_xor_sync(0xffffffffu, w, 4);
+    w += __shfl_xor_sync(0xffffffffu, w, 2);
+    w += __shfl_xor_sync(0xffffffffu, w, 1);
+    if ((lane & 7) == 0 && lane != 24) dst[lane == 0 ? 0 : (lane == 16 ? 1 : 2)] = w;
   } else {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) r[k] = warp_sum(r[k], width);
+    for (int k = 0; k < 3; ++k) r[k] = warp_sum(r[k], width);
     if (lane == 0) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) dst[k] = r[k];
+      dst[0] = r[0];
+      dst[1] = r[1];
+      dst[2] = r[2];
     }
+  }
+}
+
+// One component K of the three (structured classes): lane 0 writes it and zeroes the rest.
+template <int K, typename Real>
+__device__ __forceinline__ void warp_sum1(Real x, int lane, int width, Real* dst) {
+  x = warp_sum(x, width);
+  if (lane == 0) {
+    dst[0] = K == 0 ? x : Real(0);
+    dst[1] = K == 1 ? x : Real(0);
+    dst[2] = K == 2 ? x : Real(0);
   }
 }
 
@@ -459,9 +454,9 @@ __device__ __forceinline__ void op_bwd(const KOp& o, Cx<Real>* v, Cx<Real>* l,
     dispatch_slot<RB>(o.a, [&](auto K) {
       constexpr int k = decltype(K)::value;
       if (o.acc >= 0) {
-        Real r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        accum_r<RB, k>(v, l, r);
-        warp_sum8(r, lane, width, wacc_w + o.acc);
+        Real r[3] = {0, 0, 0};
+        accum_c3<RB, k>(v, l, r);
+        warp_sum3(r, lane, width, wacc_w + o.acc);
       }
       apply_u1_dag<RB, k>(v, m);
       apply_u1_dag<RB, k>(l, m);

@@ -222,7 +222,7 @@ int op_mats(const Op& o) {
 }
 int op_accs(const Op& o) {
   if (!o.has_param) return 0;
-  return o.type == OP_U1 ? 8 : o.nslots;
+  return o.type == OP_U1 ? 3 : o.nslots;  // U1: Pauli components (cX, cY, cZ) of R
 }
 
 struct Budget {

@@ -206,8 +206,8 @@ __global__ void finalize_kernel(const FinArgs a) {
       ctb[g.contrib] = g.factor * tot[g.acc];
       continue;
     }
-    const cdd R[4] = {{tot[g.acc + 0], tot[g.acc + 1]}, {tot[g.acc + 2], tot[g.acc + 3]},
-                      {tot[g.acc + 4], tot[g.acc + 5]}, {tot[g.acc + 6], tot[g.acc + 7]}};
+    // Pauli components of R' (device_common.cuh accum_c3): Im Tr(B R') = bx c0 + by c1 + bz c2
+    const double c3[3] = {tot[g.acc + 0], tot[g.acc + 1], tot[g.acc + 2]};
     cdd Sfx[4] = {{1, 0}, {0, 0}, {0, 0}, {1, 0}};
     for (int c = g.cons_count - 1; c >= 0; --c) {
       const DCons cn = a.cons[g.cons_begin + c];
@@ -219,11 +219,9 @@ __global__ void finalize_kernel(const FinArgs a) {
         cdd T1[4], Bm[4], Sd[4] = {cconj(Sfx[0]), cconj(Sfx[2]), cconj(Sfx[1]), cconj(Sfx[3])};
         mat2mul(Sfx, Pm, T1);
         mat2mul(T1, Sd, Bm);
-        // Tr(B R') = sum_ij B_ji R'_ij
-        cdd tr = {0, 0};
-        for (int i = 0; i < 2; ++i)
-          for (int j = 0; j < 2; ++j) tr = cadd(tr, cmul(Bm[j * 2 + i], R[i * 2 + j]));
-        ctb[cn.contrib] = cn.coeff * tr.y;
+        // B Hermitian traceless: B = bx X + by Y + bz Z, B01 = bx - i by, B00 = bz
+        const double bx = Bm[1].x, by = -Bm[1].y, bz = Bm[0].x;
+        ctb[cn.contrib] = cn.coeff * (bx * c3[0] + by * c3[1] + bz * c3[2]);
       }
       cdd G[4];
       gate1(cn, th, a.fixed, G);
@@ -516,9 +514,10 @@ double op_flops(const Op& o, bool bwd) {
   for (auto& t : o.terms) npar += t.param >= 0;
   switch (o.type) {
     case OP_U1:
-      if (u1_class(o.cons))  // structured: real scalar x complex terms, half the R' entries
-        return bwd ? 12.0 + (o.has_param ? 8.0 : 0.0) : 6.0;
-      return bwd ? 28.0 + (o.has_param ? 16.0 : 0.0) : 14.0;
+      // gradient: 3 Pauli components of R' = 12 FMA per pair (one component: 4)
+      if (u1_class(o.cons))  // structured: real scalar x complex terms
+        return bwd ? 12.0 + (o.has_param ? 4.0 : 0.0) : 6.0;
+      return bwd ? 28.0 + (o.has_param ? 12.0 : 0.0) : 14.0;
     case OP_U2F: return bwd ? 60.0 : 30.0;
     case OP_CX: return 0.0;
     default: return bwd ? 12.0 * nt + 2.0 * npar : 6.0 * nt;
