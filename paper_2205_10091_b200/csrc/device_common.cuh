@@ -212,6 +212,29 @@ __device__ __forceinline__ void tma_store(const void* tmap, const int* c, int ra
       break;
   }
 }
+// L2 prefetch of a tensor tile (no smem, no barrier): the next tile's HBM latency overlaps
+// this tile's compute.
+__device__ __forceinline__ void tma_prefetch(const void* tmap, const int* c, int rank) {
+  const uint64_t tm = (uint64_t)tmap;
+  switch (rank) {
+    case 2:
+      asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];"
+                   ::"l"(tm), "r"(c[0]), "r"(c[1]) : "memory");
+      break;
+    case 3:
+      asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];"
+                   ::"l"(tm), "r"(c[0]), "r"(c[1]), "r"(c[2]) : "memory");
+      break;
+    case 4:
+      asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];"
+                   ::"l"(tm), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]) : "memory");
+      break;
+    case 5:
+      asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];"
+                   ::"l"(tm), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]) : "memory");
+      break;
+  }
+}
 __device__ __forceinline__ void tma_store_commit_wait() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
