@@ -149,6 +149,7 @@ def main():
     ap.add_argument("--batch-qubits", type=int, default=None,
                     help="config 4: local qubits per rank (default 33)")
     ap.add_argument("--tile-bits", type=int, default=0)
+    ap.add_argument("--coalesce-bits", type=int, default=0)
     ap.add_argument("--max-ops-per-pass", type=int, default=0)
     ap.add_argument("--jit", type=int, default=1, help="1: per-circuit specialised kernels")
     ap.add_argument("--mode", default=None, choices=["grad", "expect"],
@@ -185,7 +186,8 @@ def main():
     if world > 1 and rank > 0:  # distinct seeded rows per rank (weak scaling)
         theta = W.thetas(B, circ.n_params, 1000 + rank) if args.config != 2 else \
             W.qaoa_thetas(B, 5, 1000 + rank)
-    C = tcx.Circuit(circ, dtype, tile_bits=args.tile_bits, max_ops_per_pass=args.max_ops_per_pass,
+    C = tcx.Circuit(circ, dtype, tile_bits=args.tile_bits, coalesce_bits=args.coalesce_bits,
+                    max_ops_per_pass=args.max_ops_per_pass,
                     jit=bool(args.jit))
     P = tcx.Pauli(H)
     t_jit = time.perf_counter()
@@ -327,7 +329,7 @@ def main():
                    "pauli_terms": int(len(H.weights)),
                    "l2": "inputs larger than L2 (psi+lambda %.1f GiB per GPU)" % (
                        2 * B * (2 ** circ.n) * (8 if dtype == "c64" else 16) / 2 ** 30),
-                   "plan": {k: info[k] for k in ("tile_bits", "reg_bits", "fwd_passes",
+                   "plan": {k: info[k] for k in ("tile_bits", "reg_bits", "coalesce_bits", "fwd_passes",
                                                  "lambda_passes", "bwd_passes", "stages",
                                                  "n_ops", "jit")},
                    "jit_compile_s": round(t_jit, 2), "mode": mode,

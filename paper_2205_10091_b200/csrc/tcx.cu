@@ -662,7 +662,7 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
       a.b0 = b0;
       if (jf) {
         Drv& D = drv();
-        const int ns = P.jit_nsub;
+        const int ns = jkey[0] == 'p' ? P.jit_nsub : 1;  // lambda kernels: one tile per CTA
         if (b0 == 0) {
           const TmaDims td = tma_dims(P.nloc, a.wmask, c128);
           a.use_tma = 0;
