@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 #include <complex>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
@@ -76,7 +77,11 @@ struct Lowerer {
       if (bits >> b & 1) lastS = std::max(lastS, last_on_bit[b]);
     bool par = false;
     for (auto& t : terms) par |= t.param >= 0;
-    if (last_diag >= 0 && last_diag >= lastS) {
+    // Diagonal gates stay separate ops here (a merged op would carry the union of their
+    // bits as false light-cone dependencies); runs of consecutive diagonal ops inside one
+    // pass are merged after pass scheduling (merge_pass_diagonals).
+    static const bool merge = getenv("TCX_DIAG_EARLY_MERGE") != nullptr;
+    if (merge && last_diag >= 0 && last_diag >= lastS) {
       Op& d = P.ops[last_diag];
       d.terms.insert(d.terms.end(), terms.begin(), terms.end());
       d.bits |= bits;
@@ -280,7 +285,56 @@ struct Scheduler {
     }
     return 0;
   }
+  // Window for the next pass.  Candidates come from three greedy families (score growth,
+  // earliest need, contiguous runs); with lookahead each of the best few is rolled out with
+  // the greedy choice to the end of the schedule and the one finishing in the fewest passes
+  // wins (ties: more work now).
+  bool lookahead = false;
   uint64_t choose_window() {
+    std::vector<std::pair<double, uint64_t>> cand;
+    uint64_t W0 = candidates(&cand);
+    if (!lookahead || cand.size() < 2) return W0;
+    std::sort(cand.begin(), cand.end(), [](const std::pair<double, uint64_t>& a,
+                                           const std::pair<double, uint64_t>& b) {
+      return a.first > b.first || (a.first == b.first && a.second < b.second);
+    });
+    cand.erase(std::unique(cand.begin(), cand.end(),
+                           [](const std::pair<double, uint64_t>& a, const std::pair<double, uint64_t>& b) {
+                             return a.second == b.second;
+                           }),
+               cand.end());
+    const size_t K = std::min<size_t>(cand.size(), 6);
+    const std::vector<char> done0 = done;
+    const int first0 = first;
+    int bestp = 1 << 30;
+    uint64_t bestW = W0;
+    for (size_t k = 0; k < K; ++k) {
+      uint64_t W = cand[k].second;
+      int passes = 0;
+      bool ok = true;
+      for (;;) {
+        std::vector<int> list;
+        closure(W, &list);
+        if (list.empty()) {
+          ok = false;
+          break;
+        }
+        for (int i : list) done[i] = 1;
+        while (first < (int)P.ops.size() && done[first]) first++;
+        ++passes;
+        if (first >= (int)P.ops.size() || passes >= bestp) break;
+        W = candidates(nullptr);
+      }
+      done = done0;
+      first = first0;
+      if (ok && passes < bestp) {
+        bestp = passes;
+        bestW = cand[k].second;
+      }
+    }
+    return bestW;
+  }
+  uint64_t candidates(std::vector<std::pair<double, uint64_t>>* all) {
     const int n = nl, t = P.t, c = P.c;
     if (n <= t) return (n >= 64) ? ~0ull : ((1ull << n) - 1);
     const uint64_t base = (1ull << c) - 1;
@@ -288,6 +342,7 @@ struct Scheduler {
     double best = -1;
     auto consider = [&](uint64_t W) {
       double s = closure(W, nullptr);
+      if (all) all->push_back({s, W});
       if (s > best) {
         best = s;
         bestW = W;
@@ -765,6 +820,7 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
   // ---- pass scheduling
   g_packed_u1 = dtype == TCX_C64;
   Scheduler S(P);
+  S.lookahead = gb == 0 && P.ops.size() <= 4096 && !(getenv("TCX_PLAN_GREEDY"));
   const int rb = c128 ? 8 : 4;  // bytes per Real
   S.pass_budget.mats = (24 * 1024) / rb;
   S.pass_budget.accs = 2048;
@@ -806,7 +862,33 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
     }
     while (S.first < (int)P.ops.size() && S.done[S.first]) S.first++;
     left -= list.size();
+    if (getenv("TCX_PLAN_DEBUG"))
+      fprintf(stderr, "tcx plan: pass %zu seg %d window %llx ops %zu\n", P.passes.size(), seg,
+              (unsigned long long)W, list.size());
     P.passes.push_back(std::move(pi));
+  }
+  // merge runs of consecutive diagonal ops within each pass (they commute, and no op of
+  // the pass sits between them; ops of other passes keep their order relative to the pass)
+  for (auto& pass : P.passes) {
+    std::vector<int> kept;
+    for (int i : pass.ops) {
+      Op& o = P.ops[i];
+      if (o.type == OP_DIAG && !kept.empty() && P.ops[kept.back()].type == OP_DIAG) {
+        Op& d = P.ops[kept.back()];
+        d.terms.insert(d.terms.end(), o.terms.begin(), o.terms.end());
+        d.bits |= o.bits;
+        d.has_param |= o.has_param;
+        o.terms.clear();
+        o.has_param = false;
+        o.nslots = 0;
+        o.pass = -1;
+        continue;
+      }
+      kept.push_back(i);
+    }
+    for (int i : kept)
+      if (P.ops[i].type == OP_DIAG) normalize_diag(P.ops[i]);
+    pass.ops = kept;
   }
   if (P.passes.empty() || P.passes.back().seg != seg) {  // init / trailing-layout pass
     PassInfo pi;
