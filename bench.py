@@ -150,6 +150,7 @@ def main():
                     help="config 4: local qubits per rank (default 33)")
     ap.add_argument("--tile-bits", type=int, default=0)
     ap.add_argument("--coalesce-bits", type=int, default=0)
+    ap.add_argument("--reg-bits", type=int, default=0)
     ap.add_argument("--max-ops-per-pass", type=int, default=0)
     ap.add_argument("--jit", type=int, default=1, help="1: per-circuit specialised kernels")
     ap.add_argument("--mode", default=None, choices=["grad", "expect"],
@@ -187,6 +188,7 @@ def main():
         theta = W.thetas(B, circ.n_params, 1000 + rank) if args.config != 2 else \
             W.qaoa_thetas(B, 5, 1000 + rank)
     C = tcx.Circuit(circ, dtype, tile_bits=args.tile_bits, coalesce_bits=args.coalesce_bits,
+                    reg_bits=args.reg_bits,
                     max_ops_per_pass=args.max_ops_per_pass,
                     jit=bool(args.jit))
     P = tcx.Pauli(H)

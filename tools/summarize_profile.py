@@ -54,7 +54,8 @@ def main():
     for c, v in sorted(by.items(), key=lambda x: -x[1]):
         lines.append(f"| {c} | {v / 1e6:.2f} | {v / tot:.3f} |")
     # traffic
-    tr = read_csv(os.path.join(OUT, f"traffic_{tag}.csv"))
+    tp = os.path.join(OUT, f"traffic_{tag}.csv")
+    tr = read_csv(tp) if os.path.exists(tp) else []
     m = defaultdict(dict)
     for r in tr:
         m[(int(r["ID"]), r["Kernel Name"])][r["Metric Name"]] = float(r["Metric Value"].replace(",", ""))
@@ -69,6 +70,8 @@ def main():
     lines += ["", "## DRAM traffic per launch (dram__bytes_read.sum + dram__bytes_write.sum)", "",
               "| class | launches captured | mean GB / launch |", "|---|---|---|"]
     traffic = {}
+    if not cls:
+        lines.append("| (no traffic pass this round; see the full captures below) | | |")
     for c, v in cls.items():
         lines.append(f"| {c} | {len(v)} | {sum(v) / len(v) / 1e9:.3f} |")
         traffic[c] = sum(v) / len(v)
@@ -108,8 +111,9 @@ def main():
         f.write("\n".join(lines) + "\n")
     tj = os.path.join(PROF, "traffic.json")
     allt = json.load(open(tj)) if os.path.exists(tj) else {}
-    allt[workload] = {k: v for k, v in traffic.items()}
-    allt[workload]["source"] = f"profiles/ncu_{tag}.md"
+    if traffic:
+        allt[workload] = {k: v for k, v in traffic.items()}
+        allt[workload]["source"] = f"profiles/ncu_{tag}.md"
     json.dump(allt, open(tj, "w"), indent=1)
     print("\n".join(lines))
 
