@@ -451,6 +451,37 @@ __device__ __forceinline__ void diag_term(Cx<Real>* v, const Map<RB>& mp, const 
   }
 }
 
+// one weight class (plan.cpp LUT op, KOp.a == 1): v[j] *= table[c(j)], c(j) = number of
+// terms whose signed parity (KTerm.pad = weight sign) is odd at amplitude j
+template <typename Real, int RB, bool CONJ>
+__device__ __forceinline__ void diag_lut(Cx<Real>* v, Cx<Real>* l, const Map<RB>& mp, const KOp& o,
+                                         const KTerm* terms, const Real* mats) {
+  int c[1 << RB];
+#pragma unroll
+  for (int j = 0; j < (1 << RB); ++j) c[j] = 0;
+  for (int k = 0; k < o.nterm; ++k) {
+    const KTerm tm = terms[o.term + k];
+    const uint32_t tp = (__popcll((mp.g | mp.gb) & tm.mask) & 1u) ^ (uint32_t)tm.pad;
+    const uint32_t mr = regmask<RB>(mp, tm.mask);
+#pragma unroll
+    for (int j = 0; j < (1 << RB); ++j) c[j] += (int)(tp ^ (__popc((uint32_t)j & mr) & 1u));
+  }
+  const Cx<Real>* lut = reinterpret_cast<const Cx<Real>*>(mats + terms[o.term].wofs);
+#pragma unroll
+  for (int j = 0; j < (1 << RB); ++j) {
+    const Cx<Real> ph = lut[c[j]];
+    const Real sw = CONJ ? -ph.y : ph.y;
+    Cx<Real> p = v[j];
+    v[j].x = p.x * ph.x - p.y * sw;
+    v[j].y = p.x * sw + p.y * ph.x;
+    if (l) {
+      p = l[j];
+      l[j].x = p.x * ph.x - p.y * sw;
+      l[j].y = p.x * sw + p.y * ph.x;
+    }
+  }
+}
+
 template <typename Real, int RB>
 __device__ __forceinline__ void op_fwd(const KOp& o, Cx<Real>* v, const Map<RB>& mp,
                                        const Real* mats, const KTerm* terms) {
@@ -462,7 +493,10 @@ __device__ __forceinline__ void op_fwd(const KOp& o, Cx<Real>* v, const Map<RB>&
   } else if (o.type == OP_CX) {
     op_cx<RB>(o, v, mp.g | mp.gb);
   } else if (o.type == OP_DIAG) {
-    for (int k = 0; k < o.nterm; ++k) diag_term<Real, RB, false>(v, mp, terms[o.term + k], mats);
+    if (o.a == 1)
+      diag_lut<Real, RB, false>(v, nullptr, mp, o, terms, mats);
+    else
+      for (int k = 0; k < o.nterm; ++k) diag_term<Real, RB, false>(v, mp, terms[o.term + k], mats);
   }
 }
 
@@ -512,9 +546,12 @@ __device__ __forceinline__ void op_bwd(const KOp& o, Cx<Real>* v, Cx<Real>* l,
           acc += s ? -tj : tj;
         }
       }
-      diag_term<Real, RB, true>(v, mp, tm, mats);
-      diag_term<Real, RB, true>(l, mp, tm, mats);
+      if (o.a != 1) {
+        diag_term<Real, RB, true>(v, mp, tm, mats);
+        diag_term<Real, RB, true>(l, mp, tm, mats);
+      }
     }
+    if (o.a == 1) diag_lut<Real, RB, true>(v, l, mp, o, terms, mats);
     if (cur >= 0) {
       acc = warp_sum(acc, width);
       if (lane == 0) wacc_w[cur] = acc;

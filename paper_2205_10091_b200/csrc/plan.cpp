@@ -222,7 +222,7 @@ int op_mats(const Op& o) {
     case OP_U1: return g_packed_u1 ? 32 : 8;
     case OP_U2F: return 32;
     case OP_CX: return 0;
-    default: return 2 * (int)o.terms.size();
+    default: return 2 * ((int)o.terms.size() + (o.lut ? 1 : 0));
   }
 }
 int op_accs(const Op& o) {
@@ -867,6 +867,7 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
               (unsigned long long)W, list.size());
     P.passes.push_back(std::move(pi));
   }
+  static const bool lut_off = getenv("TCX_DIAG_NOLUT") != nullptr;
   // merge runs of consecutive diagonal ops within each pass (they commute, and no op of
   // the pass sits between them; ops of other passes keep their order relative to the pass)
   for (auto& pass : P.passes) {
@@ -886,9 +887,56 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
       }
       kept.push_back(i);
     }
-    for (int i : kept)
-      if (P.ops[i].type == OP_DIAG) normalize_diag(P.ops[i]);
-    pass.ops = kept;
+    // split each merged diagonal into weight classes (param, |w|): a class of T >= 2 terms
+    // becomes a LUT op (its phase is exp(i W (T - 2c)), c = number of terms whose signed
+    // parity is odd: one table read and one complex multiply per amplitude); the rest
+    // stays a grouped op
+    std::vector<int> out;
+    for (int i : kept) {
+      if (P.ops[i].type != OP_DIAG || lut_off) {
+        if (P.ops[i].type == OP_DIAG) normalize_diag(P.ops[i]);
+        out.push_back(i);
+        continue;
+      }
+      normalize_diag(P.ops[i]);
+      std::map<std::pair<int, double>, std::vector<DiagTerm>> cls;
+      for (auto& tm : P.ops[i].terms) cls[{tm.param, std::fabs(tm.w)}].push_back(tm);
+      std::vector<DiagTerm> rest;
+      std::vector<Op> luts;
+      for (auto& kv : cls) {
+        if (kv.second.size() < 2 || kv.first.second == 0.0) {
+          rest.insert(rest.end(), kv.second.begin(), kv.second.end());
+          continue;
+        }
+        Op L;
+        L.type = OP_DIAG;
+        L.lut = true;
+        L.need = 0;
+        L.pass = P.ops[i].pass;
+        for (auto& tm : kv.second) L.bits |= tm.mask;
+        L.terms = kv.second;
+        normalize_diag(L);
+        luts.push_back(std::move(L));
+      }
+      if (!rest.empty()) {
+        Op& d = P.ops[i];
+        d.terms = rest;
+        d.bits = 0;
+        for (auto& tm : rest) d.bits |= tm.mask;
+        normalize_diag(d);
+        out.push_back(i);
+      } else {
+        P.ops[i].terms.clear();
+        P.ops[i].has_param = false;
+        P.ops[i].nslots = 0;
+        P.ops[i].pass = -1;
+      }
+      for (auto& L : luts) {
+        out.push_back((int)P.ops.size());
+        P.ops.push_back(std::move(L));
+      }
+    }
+    pass.ops = out;
   }
   if (P.passes.empty() || P.passes.back().seg != seg) {  // init / trailing-layout pass
     PassInfo pi;
@@ -971,12 +1019,14 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
         } else {
           ko.nterm = (int16_t)o.terms.size();
           ko.term = (int)P.kterms.size() - pass.kterm_begin;
+          ko.a = o.lut ? 1 : 0;  // JIT: table-driven phase (one weight class)
           for (size_t i = 0; i < o.terms.size(); ++i) {
             KTerm kt;
             std::memset(&kt, 0, sizeof(kt));
             kt.mask = o.terms[i].mask;
-            kt.wofs = (int16_t)(mat - pass.mat_begin + 2 * (int)i);
+            kt.wofs = (int16_t)(mat - pass.mat_begin + (o.lut ? 0 : 2 * (int)i));
             kt.acc = o.terms[i].param >= 0 ? (int16_t)(stage_acc + o.terms[i].slot) : -1;
+            kt.pad = o.lut && o.terms[i].w < 0 ? 1 : 0;  // LUT: sign of the term's weight
             P.kterms.push_back(kt);
           }
         }
@@ -1054,6 +1104,19 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
       mi.payload = o.u2_payload;
       mi.param = -1;
       P.mitems.push_back(mi);
+    } else if (o.type == OP_DIAG && o.lut) {
+      // table entry c = exp(i W (T - 2c)) for c odd-signed terms, W = |w| of the class
+      const int T = (int)o.terms.size();
+      const double W = std::fabs(o.terms[0].w);
+      for (int cnt = 0; cnt <= T; ++cnt) {
+        MItem mi{};
+        mi.type = OP_DIAG;
+        mi.mat_off = o.mat_off + 2 * cnt;
+        mi.param = o.terms[0].param;
+        mi.w = W * (double)(T - 2 * cnt);
+        mi.payload = -1;
+        P.mitems.push_back(mi);
+      }
     } else if (o.type == OP_DIAG) {
       for (size_t i = 0; i < o.terms.size(); ++i) {
         MItem mi{};
@@ -1064,6 +1127,8 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
         mi.payload = -1;
         P.mitems.push_back(mi);
       }
+    }
+    if (o.type == OP_DIAG) {
       // one finalize item per gradient slot
       std::vector<int> seen(o.nslots, 0);
       for (auto& tm : o.terms) {

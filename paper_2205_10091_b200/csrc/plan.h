@@ -50,6 +50,7 @@ struct Op {
   std::vector<DiagTerm> terms;    // DIAG
   int nslots = 0;                 // DIAG: distinct gradient slots
   bool has_param = false;
+  bool lut = false;  // DIAG: one weight class (param, |w|); phase from a (T+1)-entry table
   // layout (filled by the scheduler)
   int pass = -1;
   int mat_off = 0, mat_len = 0;  // Reals in the per-theta table
