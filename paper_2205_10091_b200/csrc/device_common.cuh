@@ -146,6 +146,14 @@ __device__ __forceinline__ q64 qmul(q64 a, q64 b) {
 }
 
 // ---- TMA (cp.async.bulk.tensor) + mbarrier helpers for tile I/O -----------------------
+// Opaque copy: the compiler cannot hoist values computed from it out of the tile loop, so
+// per-transition shared-memory addresses are recomputed where used instead of being kept
+// live (and spilled) across the whole straight-line pass body.
+__device__ __forceinline__ uint32_t opq(uint32_t x) {
+  uint32_t r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(x));
+  return r;
+}
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }

@@ -165,7 +165,7 @@ class Circuit:
         self.h = h
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and _lib is not None:  # not during interpreter teardown
             _lib.tcx_circuit_free(self.h)
             self.h = None
 
@@ -217,7 +217,7 @@ class Pauli:
         self.h = h
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and _lib is not None:
             _lib.tcx_pauli_free(self.h)
             self.h = None
 
