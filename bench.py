@@ -99,10 +99,13 @@ class ClockSampler:
 
 
 # -------------------------------------------------------------- reference
-def cpu_oracle_rows(circ, H, theta, threads):
+def cpu_oracle_rows(circ, H, theta, threads, mode="grad"):
     from oracle import oracle as orc
     t0 = time.perf_counter()
-    orc.value_grad_batch(circ, H, theta, nthreads=threads)
+    if mode == "grad":
+        orc.value_grad_batch(circ, H, theta, nthreads=threads)
+    else:
+        orc.expect_batch(circ, H, theta, nthreads=threads)
     return time.perf_counter() - t0
 
 
@@ -111,14 +114,15 @@ def run_reference(args, rank, world):
     if rank != 0:
         return 0
     name, circ, H, theta, dtype = W.config(args.config, B=args.batch)
+    mode = args.mode or ("expect" if circ.n_params == 0 else "grad")
     cores = os.cpu_count() or 1
     rows = max(1, min(cores, args.ref_rows))
     sample = theta[:rows]
     for _ in range(args.warmup):
-        cpu_oracle_rows(circ, H, sample[:1], 1)
+        cpu_oracle_rows(circ, H, sample[:1], 1, mode)
     total = 0.0
     for _ in range(args.steps):
-        total += cpu_oracle_rows(circ, H, sample, rows)
+        total += cpu_oracle_rows(circ, H, sample, rows, mode)
     value = rows * args.steps / total
     unit = "circuits/s"
     line = {
@@ -313,7 +317,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
         rows = max(1, min(cores, args.cpu_rows))
-        secs = cpu_oracle_rows(circ, H, theta[:rows], rows)
+        secs = cpu_oracle_rows(circ, H, theta[:rows], rows, mode)
         cpu = {"value": rows / secs, "unit": "circuits/s", "cores": rows, "kind": "oracle",
                "sample": f"{rows} theta rows of {name} (one OpenMP thread per row), {secs:.1f} s"}
 

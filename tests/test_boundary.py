@@ -145,3 +145,18 @@ def test_no_cpu_fallback(tcx):
                                  ctypes.cast(buf, ctypes.c_void_p), len(buf), None)
     assert rc == 4, tcx.last_error()
     assert "no CUDA device" in tcx.last_error()
+
+
+def test_bench_reference_arm_runs():
+    """`bench.py --impl reference` (the tier's reference arm: the CPU oracle) prints one
+    JSON line with the contract keys (small config, CPU only)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference",
+                          "--config", "0", "--steps", "1", "--warmup", "1"],
+                         capture_output=True, text=True, timeout=300, check=True).stdout
+    line = json.loads(out.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "oracle" and line["e2e"]["h2d_bytes_per_step"] == 0
