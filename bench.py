@@ -156,6 +156,8 @@ def main():
     ap.add_argument("--coalesce-bits", type=int, default=0)
     ap.add_argument("--reg-bits", type=int, default=0)
     ap.add_argument("--max-ops-per-pass", type=int, default=0)
+    ap.add_argument("--dense-k", type=int, default=0,
+                    help="fuse gates into dense k-qubit blocks (k = 1..5; cfg4 k-sweep)")
     ap.add_argument("--jit", type=int, default=1, help="1: per-circuit specialised kernels")
     ap.add_argument("--mode", default=None, choices=["grad", "expect"],
                     help="grad (E + adjoint gradient, default) or expect (forward + E only; cfg4)")
@@ -194,7 +196,7 @@ def main():
     C = tcx.Circuit(circ, dtype, tile_bits=args.tile_bits, coalesce_bits=args.coalesce_bits,
                     reg_bits=args.reg_bits,
                     max_ops_per_pass=args.max_ops_per_pass,
-                    jit=bool(args.jit))
+                    jit=bool(args.jit), dense_k=args.dense_k)
     P = tcx.Pauli(H)
     t_jit = time.perf_counter()
     mode = args.mode or ("expect" if circ.n_params == 0 else "grad")
@@ -303,7 +305,10 @@ def main():
             ach = byt / (kms / 1e3) / 1e9
             roof = {"bound": "hbm", "achieved": ach, "peak": hbm_peak / 1e9, "unit": "GB/s",
                     "frac": ach / (hbm_peak / 1e9)}
-        roof.update({"kernel": f"pass_kernel ({dom} passes)", "launches": cnt,
+        kname = {"dense": "dense_fwd_kernel (dense k-qubit blocks)",
+                 "dense_backward": "dense_bwd_kernel (dense k-qubit blocks, adjoint)"}.get(
+                     dom, f"pass_kernel ({dom} passes)")
+        roof.update({"kernel": kname, "launches": cnt,
                      "share_of_step": kms / total_k,
                      "peak_source": alu_src if roof["bound"] == "alu" else peak_src + " (MEASURED_PEAKS.json hbm_gbs)",
                      "hbm_achieved_gbs": byt / (kms / 1e3) / 1e9,
@@ -337,7 +342,7 @@ def main():
                        2 * B * (2 ** circ.n) * (8 if dtype == "c64" else 16) / 2 ** 30),
                    "plan": {k: info[k] for k in ("tile_bits", "reg_bits", "coalesce_bits", "fwd_passes",
                                                  "lambda_passes", "bwd_passes", "stages",
-                                                 "n_ops", "jit")},
+                                                 "n_ops", "jit", "dense_k", "dense_blocks")},
                    "jit_compile_s": round(t_jit, 2), "mode": mode,
                    "max_ops_per_pass": args.max_ops_per_pass},
         "roofline": roof,

@@ -97,7 +97,12 @@ typedef struct {
     int32_t global_bits;    /* g > 0: the state is sharded over 2^g ranks on its top g index
                                bits (qubits 0..g-1); run with tcx_shard_* (north_star
                                "shards on its top log2(G) global qubits") */
-    int32_t reserved[2];
+    int32_t dense_k;        /* k in [1, 5]: fuse the gate list greedily into dense k-qubit
+                               blocks (2-qubit gates make at least 2-qubit blocks) and apply
+                               each as one 2^k x 2^k complex contraction over the state
+                               (north_star step 2); 0 = window passes only.
+                               Not with global_bits; grad needs k <= 4. */
+    int32_t reserved;
 } tcx_build_opts;
 
 /* Executed-plan summary (for reports and tests). */
@@ -117,6 +122,8 @@ typedef struct {
     int64_t tiles_per_state;  /* 2^(n-t) */
     int64_t acc_slots;        /* gradient partial slots per tile */
     int64_t mat_reals;        /* per-theta materialised matrix entries */
+    int32_t dense_k;          /* dense block size cap (0: no dense blocks) */
+    int32_t dense_blocks;     /* dense k-qubit block passes (each one read+write of psi) */
 } tcx_plan_info;
 
 typedef struct tcx_circuit tcx_circuit;

@@ -16,6 +16,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <array>
+#include <functional>
 #include <set>
 
 namespace tcx {
@@ -637,6 +639,118 @@ void shard_swap_perm(int n, int g, int* perm) {
   }
 }
 
+// Dense k-qubit block fusion (north_star step 2 "fused k-qubit blocks run
+// as small dense complex contractions").  Greedy, in program order: every open block owns
+// a disjoint set of physical bits; a gate joins (merging every open block it touches) when
+// the union stays within k bits, else the blocks it touches are closed and emitted and
+// the gate opens a new block (at k = 1 a 2-qubit gate is a block of its own; the cfg4
+// brick circuit gives 8702 / 2999 / 2696 / 1500 / 1137 blocks for k = 1..5).  Per bit, blocks are emitted in program order,
+// and blocks on disjoint bits commute, so the emitted sequence equals the gate list.
+// SWAP stays a relabel of the qubit -> bit map (as in the window lowering).
+void build_dense(Plan& P, const tcx_gate* gates, int64_t G, int* pos,
+                 const std::function<int64_t(int64_t, int)>& payload_copy) {
+  struct Open {
+    std::vector<int64_t> g;
+    uint64_t mask = 0;
+    int64_t order = 0;
+  };
+  std::vector<Open> open;
+  std::vector<std::array<int, 2>> gp((size_t)G);  // physical bits of each gate when it ran
+  auto pos_at = [&](int64_t gi) { return gp[(size_t)gi].data(); };
+  auto emit = [&](const Open& o) {
+    DBlock d{};
+    d.k = popc64(o.mask);
+    int loc[64];
+    int i = 0;
+    for (int b = 0; b < P.n; ++b)
+      if (o.mask >> b & 1) {
+        loc[b] = i;
+        d.bits[i++] = b;
+      }
+    d.gate_begin = (int)P.dgates.size();
+    d.gate_count = (int)o.g.size();
+    for (int64_t gi : o.g) {
+      const tcx_gate& x = gates[gi];
+      DGate dg{};
+      dg.kind = x.kind;
+      dg.a = loc[pos_at(gi)[0]];
+      dg.b = is_2q(x.kind) ? loc[pos_at(gi)[1]] : -1;
+      dg.param = is_rot(x.kind) ? x.param : -1;
+      dg.coeff = x.coeff;
+      dg.payload = -1;
+      if (x.kind == TCX_U1) dg.payload = payload_copy(x.payload, 2);
+      if (x.kind == TCX_U2) dg.payload = payload_copy(x.payload, 4);
+      dg.contrib = -1;
+      d.has_param |= dg.param >= 0;
+      P.dgates.push_back(dg);
+    }
+    d.shared = d.has_param ? 0 : 1;
+    const int m = 1 << (2 * d.k);
+    if (d.shared) {
+      d.mat_off = P.dmat_shared;
+      P.dmat_shared += m;
+    } else {
+      d.mat_off = P.dmat_row;
+      P.dmat_row += m;
+    }
+    d.acc_off = -1;
+    if (d.has_param) {  // R' = sum psi_out lam_out^dagger: 2^(2k) complex (re, im)
+      d.acc_off = P.dacc_total;
+      P.dacc_total += 2 * m;
+    }
+    P.dblocks.push_back(d);
+  };
+  int64_t order = 0;
+  for (int64_t gi = 0; gi < G; ++gi) {
+    const tcx_gate& x = gates[gi];
+    if (x.kind == TCX_I) continue;
+    if (x.kind == TCX_SWAP) {
+      std::swap(pos[x.q0], pos[x.q1]);
+      P.relabeled = true;
+      continue;
+    }
+    const int ar = is_2q(x.kind) ? 2 : 1;
+    int* pp = pos_at(gi);
+    pp[0] = pos[x.q0];
+    pp[1] = ar == 2 ? pos[x.q1] : -1;
+    const uint64_t Q = (1ull << pp[0]) | (ar == 2 ? (1ull << pp[1]) : 0ull);
+    uint64_t U = Q;
+    std::vector<size_t> touch;
+    for (size_t i = 0; i < open.size(); ++i)
+      if (open[i].mask & Q) {
+        touch.push_back(i);
+        U |= open[i].mask;
+      }
+    std::sort(touch.begin(), touch.end(),
+              [&](size_t a, size_t b) { return open[a].order < open[b].order; });
+    if (popc64(U) <= P.dense_k) {
+      Open m;
+      m.order = touch.empty() ? order++ : open[touch[0]].order;
+      for (size_t i : touch) m.g.insert(m.g.end(), open[i].g.begin(), open[i].g.end());
+      m.g.push_back(gi);
+      m.mask = U;
+      std::vector<Open> keep;
+      for (size_t i = 0; i < open.size(); ++i)
+        if (!(open[i].mask & Q)) keep.push_back(std::move(open[i]));
+      keep.push_back(std::move(m));
+      open.swap(keep);
+      continue;
+    }
+    for (size_t i : touch) emit(open[i]);
+    std::vector<Open> keep;
+    for (size_t i = 0; i < open.size(); ++i)
+      if (!(open[i].mask & Q)) keep.push_back(std::move(open[i]));
+    Open nb;
+    nb.g.push_back(gi);
+    nb.mask = Q;
+    nb.order = order++;
+    keep.push_back(std::move(nb));
+    open.swap(keep);
+  }
+  std::sort(open.begin(), open.end(), [](const Open& a, const Open& b) { return a.order < b.order; });
+  for (auto& o : open) emit(o);
+}
+
 tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const double* mats,
                       int64_t nmat, tcx_dtype dtype, const tcx_build_opts* opts, Plan& P,
                       std::string& err) {
@@ -720,6 +834,19 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
   P.c = c;
   P.h = t - r;
   P.max_ops_per_pass = opts ? std::max(0, opts->max_ops_per_pass) : 0;
+  P.dense_k = opts ? opts->dense_k : 0;
+  if (P.dense_k < 0 || P.dense_k > kMaxDenseK) {
+    err = "dense_k must be in [0, 5]";
+    return TCX_E_INVALID;
+  }
+  if (P.dense_k > 0 && gb > 0) {
+    err = "dense_k is not supported with global_bits (sharded state)";
+    return TCX_E_UNSUPPORTED;
+  }
+  if (P.dense_k > 0 && n < 2) {
+    err = "dense_k needs n_qubits >= 2";
+    return TCX_E_INVALID;
+  }
   P.tiles = 1ll << (n - gb - t);
   P.tpc = (int)std::min<int64_t>(64, std::max<int64_t>(1, P.tiles / 32));
   // two lock-stepped sub-tiles (512 threads) share one instruction stream in the JIT
@@ -737,7 +864,8 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
     if (!unitary_check(mats + 2 * off, d)) P.unitary = false;
     return at;
   };
-  for (int64_t g = 0; g < G; ++g) {
+  if (P.dense_k > 0) build_dense(P, gates, G, pos, payload_copy);
+  for (int64_t g = 0; g < G && P.dense_k == 0; ++g) {
     const tcx_gate& x = gates[g];
     if (!is_2q(x.kind)) {
       if (x.kind == TCX_I) continue;
@@ -1144,6 +1272,11 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
       }
     }
   }
+  for (auto& dg : P.dgates)
+    if (dg.param >= 0) {
+      dg.contrib = contrib++;
+      contrib_param.push_back(dg.param);
+    }
   P.n_contrib = contrib;
   P.param_ptr.assign(Pn + 1, 0);
   for (int p : contrib_param) P.param_ptr[p + 1]++;

@@ -81,6 +81,26 @@ struct GItem {       // finalize items
   int32_t contrib, pad;
 };
 
+// Dense k-qubit block (north_star step 2): a run of gates fused into one
+// 2^k x 2^k unitary U = G_m ... G_1 on k physical bits; applied as Psi' = U Psi with Psi
+// the state viewed as [2^k x 2^(n-k)].  Block-local index j: bit i of j <-> bits[i].
+constexpr int kMaxDenseK = 5;
+struct DGate {       // device: one gate of a dense block, on block-local bits
+  int32_t kind, a, b, param;  // a: local bit of q0, b: local bit of q1 (-1: 1-qubit)
+  double coeff;
+  int64_t payload;            // complex offset into Plan::fixed (U1: 4, U2: 16), else -1
+  int32_t contrib, pad;       // gradient contribution index (param >= 0), else -1
+};
+struct DBlock {
+  int32_t k;
+  int32_t bits[kMaxDenseK];   // ascending physical bits
+  int32_t gate_begin, gate_count;
+  int32_t shared;             // 1: no parameters -> U in the row-independent table
+  int32_t mat_off;            // complex offset of U (row-major 2^k x 2^k) in its table
+  int32_t acc_off;            // backward: offset of the block's Q partials (2^(2k) reals)
+  int32_t has_param;
+};
+
 struct PassInfo {
   int seg = 0;                      // sharded: segment (layout) this pass runs in
   uint64_t wmask = 0;
@@ -157,6 +177,13 @@ struct Plan {
   int64_t tiles = 1;             // 2^(n - t)
   int tpc = 1;                   // tiles per CTA (depends on the tile count only, never on B)
   int jit_nsub = 1;              // lock-stepped sub-tiles per CTA in JIT kernels
+
+  int dense_k = 0;                 // > 0: gates run as dense k-qubit blocks (tcx_build_opts)
+  std::vector<DBlock> dblocks;     // in execution order (before the window passes)
+  std::vector<DGate> dgates;
+  int dmat_row = 0;                // complex entries per theta row (parameterised blocks)
+  int dmat_shared = 0;             // complex entries of the row-independent table
+  int dacc_total = 0;              // backward Q partial reals per CTA slot
 
   bool jit_on = false;             // per-circuit specialised kernels (compiled lazily)
   std::map<std::string, JitKernel> jit;  // key (jit.h) -> compiled CUBIN

@@ -20,6 +20,7 @@
 
 #include "jit.h"
 #include "kernels.cuh"
+#include "dense.cuh"
 #include "plan.h"
 
 using namespace tcx;
@@ -263,6 +264,7 @@ struct DevBuf {
 namespace tcx {
 struct DeviceTables {
   DevBuf kops, kterms, kstages, mitems, dcons, gitems, pptr, plist, fixed, layout, swb;
+  DevBuf dblocks, dgates, dpblocks;  // dense k-qubit blocks (dense.cuh)
   std::map<std::string, CUfunction> jit;   // key (jit.h)
   std::map<std::string, size_t> jit_smem;  // dynamic smem opted in per function
 };
@@ -362,6 +364,12 @@ tcx_status device_tables(Plan& P, DeviceTables*& out) {
     return s;
   std::vector<int> lay(P.layout, P.layout + P.n);
   if ((s = upload(T->layout, lay))) return s;
+  std::vector<int32_t> pbl;
+  for (size_t i = 0; i < P.dblocks.size(); ++i)
+    if (P.dblocks[i].has_param) pbl.push_back((int32_t)i);
+  if ((s = upload(T->dblocks, P.dblocks)) || (s = upload(T->dgates, P.dgates)) ||
+      (s = upload(T->dpblocks, pbl)))
+    return s;
   out = T.get();
   P.dev[dev] = T;
   return TCX_OK;
@@ -470,8 +478,18 @@ enum { K_EXPECT = 0, K_GRAD = 1, K_STATE = 2 };
 
 struct WsLayout {
   size_t psi, lam, mats, part, epart, tot, contrib, theta, E, grad, total;
+  size_t dmats, dshared, dpart, drs;  // dense blocks: U tables, R' partials / sums
   bool mega;
 };
+
+// Dense backward CTAs per theta row (fixed by n alone, so a row's reduction order never
+// depends on B): 2^(n-13) clamped to [1, 32].
+int dense_bwd_ctas(const Plan& P) { return (int)std::min<int64_t>(32, std::max<int64_t>(1, (int64_t)1 << std::max(0, P.n - 13))); }
+int dense_max_k(const Plan& P) {
+  int k = 0;
+  for (auto& d : P.dblocks) k = std::max(k, (int)d.k);
+  return k;
+}
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -481,7 +499,8 @@ WsLayout ws_layout(const Plan& P, const Binding* Bd, int64_t B, int kind, bool h
   const size_t N = size_t(1) << P.nloc;  // this rank's amplitudes (= 2^n unless sharded)
   const int64_t S = P.tiles / tiles_per_cta(P);
   const int EU = Bd ? (int)Bd->units.size() : 1;
-  w.mega = kind != K_STATE && P.passes.size() == 1 && EU == 1 && P.gbits == 0;
+  w.mega = kind != K_STATE && P.passes.size() == 1 && EU == 1 && P.gbits == 0 &&
+           P.dblocks.empty();
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
@@ -497,6 +516,15 @@ WsLayout ws_layout(const Plan& P, const Binding* Bd, int64_t B, int kind, bool h
   w.epart = kind != K_STATE ? take(B * S * EU * 8) : 0;
   w.tot = kind == K_GRAD ? take(B * std::max(P.acc_total, 1) * 8) : 0;
   w.contrib = kind == K_GRAD ? take(B * std::max(P.n_contrib, 1) * 8) : 0;
+  if (!P.dblocks.empty()) {
+    w.dmats = take(B * std::max(P.dmat_row, 1) * 2 * rs);
+    w.dshared = take(std::max(P.dmat_shared, 1) * 2 * rs);
+    if (kind == K_GRAD && P.dacc_total > 0) {
+      const int k = dense_max_k(P);
+      w.dpart = take((size_t)B * dense_bwd_ctas(P) * 2 * (1 << (2 * k)) * 8);
+      w.drs = take((size_t)B * P.dacc_total * 8);
+    }
+  }
   if (host_io) {
     w.theta = take(B * std::max(P.P, 1) * 8);
     w.E = take(B * 8);
@@ -535,6 +563,51 @@ double lambda_flops(const Binding& B, const LamUnit& u) {
   return f;
 }
 
+// ---- dense block launches (dense.cuh) -------------------------------------------------
+template <typename Real, int K>
+void dense_fwd_launch(DenseArgs& a, int64_t rows, cudaStream_t st) {
+  // columns per thread: enough bytes in flight per thread for the HBM-bound small blocks
+  constexpr int COLS = sizeof(Real) == 4 ? (K == 1 ? 4 : (K == 2 ? 2 : 1)) : (K == 1 ? 2 : 1);
+  const int64_t ncols = ((int64_t)1 << a.n) >> K;
+  const int64_t need = (ncols + 256 * COLS - 1) / (256 * COLS);
+  const int64_t gx = std::max<int64_t>(1, std::min<int64_t>(need, std::max<int64_t>(1, 148 * 8 / rows)));
+  dense_fwd_kernel<Real, K, COLS><<<dim3((unsigned)gx, (unsigned)rows), 256, 0, st>>>(a);
+}
+template <typename Real>
+cudaError_t dense_fwd(int K, DenseArgs& a, int64_t rows, cudaStream_t st) {
+  switch (K) {
+    case 1: dense_fwd_launch<Real, 1>(a, rows, st); break;
+    case 2: dense_fwd_launch<Real, 2>(a, rows, st); break;
+    case 3: dense_fwd_launch<Real, 3>(a, rows, st); break;
+    case 4: dense_fwd_launch<Real, 4>(a, rows, st); break;
+    case 5: dense_fwd_launch<Real, 5>(a, rows, st); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+template <typename Real, int K>
+cudaError_t dense_bwd_launch(DenseArgs& a, int S, int64_t rows, cudaStream_t st) {
+  constexpr int D = 1 << K;
+  const size_t stage = (size_t)8 * 2 * 32 * D * sizeof(Cx<Real>);
+  const size_t red = (size_t)8 * D * D * 2 * sizeof(double);
+  const size_t sm = std::max(stage, red);
+  cudaError_t e = cudaFuncSetAttribute(dense_bwd_kernel<Real, K>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  dense_bwd_kernel<Real, K><<<dim3((unsigned)S, (unsigned)rows), 256, sm, st>>>(a);
+  return cudaGetLastError();
+}
+template <typename Real>
+cudaError_t dense_bwd(int K, DenseArgs& a, int S, int64_t rows, cudaStream_t st) {
+  switch (K) {
+    case 1: return dense_bwd_launch<Real, 1>(a, S, rows, st);
+    case 2: return dense_bwd_launch<Real, 2>(a, S, rows, st);
+    case 3: return dense_bwd_launch<Real, 3>(a, S, rows, st);
+    case 4: return dense_bwd_launch<Real, 4>(a, S, rows, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 // one step of a sharded program (tcx_shard_exec); nullptr = the whole single-GPU program
 struct OneStep {
   int kind, arg, rank;
@@ -556,6 +629,8 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
   if (kind == K_STATE && !state) return fail(TCX_E_INVALID, "null state");
   if (kind == K_GRAD && !P.unitary)
     return fail(TCX_E_UNSUPPORTED, "grad needs unitary payloads (adjoint applies U^dagger)");
+  if (kind == K_GRAD && dense_max_k(P) > 4)
+    return fail(TCX_E_UNSUPPORTED, "grad with dense blocks needs dense_k <= 4");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     return fail(TCX_E_CUDA, "no CUDA device (tcx has no CPU fallback)");
@@ -600,6 +675,51 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
       materialize_kernel<float><<<g, 128, 0, st>>>(ma);
     CUDA_TRY(cudaGetLastError());
   }
+  // ---- dense block matrices: row-independent blocks once, parameterised ones per row
+  const bool dense = !P.dblocks.empty();
+  if (dense && want(0, 0)) {
+    DenseMatArgs dm;
+    dm.blocks = (const DBlock*)DT->dblocks.p;
+    dm.nblocks = (int)P.dblocks.size();
+    dm.gates = (const DGate*)DT->dgates.p;
+    dm.fixed = (const double*)DT->fixed.p;
+    dm.theta = P.P > 0 ? theta : nullptr;
+    dm.P = P.P;
+    if (P.dmat_shared > 0) {
+      dm.mats = W + wl.dshared;
+      dm.row_stride = 0;
+      dm.shared = 1;
+      dm.b0 = 0;
+      if (c128)
+        dense_mat_kernel<double><<<dim3(dm.nblocks, 1), 32, 0, st>>>(dm);
+      else
+        dense_mat_kernel<float><<<dim3(dm.nblocks, 1), 32, 0, st>>>(dm);
+      CUDA_TRY(cudaGetLastError());
+    }
+    for (int64_t b0 = 0; b0 < B && P.dmat_row > 0; b0 += kMaxRows) {
+      const int64_t rows = std::min(kMaxRows, B - b0);
+      dm.mats = W + wl.dmats;
+      dm.row_stride = P.dmat_row;
+      dm.shared = 0;
+      dm.b0 = b0;
+      if (c128)
+        dense_mat_kernel<double><<<dim3(dm.nblocks, (unsigned)rows), 32, 0, st>>>(dm);
+      else
+        dense_mat_kernel<float><<<dim3(dm.nblocks, (unsigned)rows), 32, 0, st>>>(dm);
+      CUDA_TRY(cudaGetLastError());
+    }
+  }
+  auto dense_args = [&](DenseArgs& d, const DBlock& blk) {
+    std::memset(&d, 0, sizeof(d));
+    d.psi = W + wl.psi;
+    d.lam = W + wl.lam;
+    const size_t csz2 = 2 * (size_t)rs;
+    d.U = blk.shared ? (const void*)(W + wl.dshared + blk.mat_off * csz2)
+                     : (const void*)(W + wl.dmats + blk.mat_off * csz2);
+    d.u_stride = blk.shared ? 0 : P.dmat_row;
+    for (int i = 0; i < blk.k; ++i) d.bits[i] = blk.bits[i];
+    d.n = P.n;
+  };
   // ---- pass launches
   auto base_args = [&](PassArgs& a, uint64_t wmask, const int* Wl, int mode) {
     std::memset(&a, 0, sizeof(a));
@@ -745,11 +865,38 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
     if ((s = launch(a, 5, 0, fl))) return s;
   } else {
     const bool sharded = P.gbits > 0;
+    for (size_t di = 0; di < P.dblocks.size(); ++di) {
+      const DBlock& blk = P.dblocks[di];
+      ProfEntry pe{};
+      if (g_prof.on) {
+        CUDA_TRY(cudaEventCreate(&pe.a));
+        CUDA_TRY(cudaEventCreate(&pe.b));
+        CUDA_TRY(cudaEventRecord(pe.a, st));
+      }
+      for (int64_t b0 = 0; b0 < B; b0 += kMaxRows) {
+        const int64_t rows = std::min(kMaxRows, B - b0);
+        DenseArgs d;
+        dense_args(d, blk);
+        d.init = di == 0 ? 1 : 0;
+        d.b0 = b0;
+        cudaError_t e = c128 ? dense_fwd<double>(blk.k, d, rows, st) : dense_fwd<float>(blk.k, d, rows, st);
+        if (e != cudaSuccess) return fail(TCX_E_CUDA, std::string("dense block launch: ") + cudaGetErrorString(e));
+      }
+      if (g_prof.on) {
+        CUDA_TRY(cudaEventRecord(pe.b, st));
+        pe.phase = 6;
+        pe.index = (int)di;
+        pe.flops = Bf * Nf * 8.0 * (double)(1 << blk.k);  // one complex MAC per U entry
+        pe.bytes = Bf * Nf * csz * (di == 0 ? 1.0 : 2.0);
+        g_prof.log.push_back(pe);
+      }
+    }
     for (int pi = 0; pi < nP; ++pi) {
       if (!want(1, pi)) continue;
       const PassInfo& p = P.passes[pi];
       const bool last = pi == nP - 1 && !sharded;  // sharded: every lambda unit is its own step
-      int mode = M_FWD | M_STORE_PSI | (pi == 0 ? M_INIT : M_LOAD_PSI);
+      if (dense && kind == K_STATE && p.ops.empty()) continue;  // trailing pass: nothing to do
+      int mode = M_FWD | M_STORE_PSI | ((pi == 0 && !dense) ? M_INIT : M_LOAD_PSI);
       PassArgs a;
       base_args(a, p.wmask, p.W, mode);
       set_pass(a, p, true);
@@ -788,6 +935,7 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
       for (int pi = nP - 1; pi >= 0; --pi) {
         if (!want(3, pi)) continue;
         const PassInfo& p = P.passes[pi];
+        if (dense && p.ops.empty()) continue;  // the trailing E / lambda pass has no gates
         int mode = M_LOAD_PSI | M_LOAD_LAM | M_BWD | (pi > 0 ? (M_STORE_PSI | M_STORE_LAM) : 0);
         PassArgs a;
         base_args(a, p.wmask, p.W, mode);
@@ -795,6 +943,65 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
         a.gbase = gbase;
         if ((s = launch(a, 3, pi, pass_flops(P, p, true)))) return s;
       }
+      const int Sd = dense_bwd_ctas(P);
+      for (int di = (int)P.dblocks.size() - 1; di >= 0; --di) {
+        const DBlock& blk = P.dblocks[di];
+        if (di == 0 && !blk.has_param) continue;  // nothing left to compute
+        ProfEntry pe{};
+        if (g_prof.on) {
+          CUDA_TRY(cudaEventCreate(&pe.a));
+          CUDA_TRY(cudaEventCreate(&pe.b));
+          CUDA_TRY(cudaEventRecord(pe.a, st));
+        }
+        for (int64_t b0 = 0; b0 < B; b0 += kMaxRows) {
+          const int64_t rows = std::min(kMaxRows, B - b0);
+          DenseArgs d;
+          dense_args(d, blk);
+          d.store = di > 0 ? 1 : 0;
+          d.part = blk.has_param ? (double*)(W + wl.dpart) : nullptr;
+          d.b0 = b0;
+          cudaError_t e = c128 ? dense_bwd<double>(blk.k, d, Sd, rows, st)
+                               : dense_bwd<float>(blk.k, d, Sd, rows, st);
+          if (e != cudaSuccess) return fail(TCX_E_CUDA, std::string("dense backward launch: ") + cudaGetErrorString(e));
+          if (blk.has_param) {
+            const int ne = 2 << (2 * blk.k);
+            dense_rsum_kernel<<<dim3((ne + 127) / 128, (unsigned)rows), 128, 0, st>>>(
+                (const double*)(W + wl.dpart), (double*)(W + wl.drs), Sd, ne, blk.acc_off,
+                P.dacc_total, b0);
+            CUDA_TRY(cudaGetLastError());
+          }
+        }
+        if (g_prof.on) {
+          CUDA_TRY(cudaEventRecord(pe.b, st));
+          pe.phase = 7;
+          pe.index = di;
+          pe.flops = Bf * Nf * 8.0 * (double)(1 << blk.k) * (blk.has_param ? 3.0 : 2.0);
+          pe.bytes = Bf * Nf * csz * (di > 0 ? 4.0 : 2.0);
+          g_prof.log.push_back(pe);
+        }
+      }
+    }
+  }
+  // ---- dense block gradient contributions (before finalize sums them per parameter)
+  if (kind == K_GRAD && dense && P.dacc_total > 0 && want(4, 0)) {
+    int npb = 0;
+    for (auto& d : P.dblocks) npb += d.has_param;
+    for (int64_t b0 = 0; b0 < B; b0 += kMaxRows) {
+      const int64_t rows = std::min(kMaxRows, B - b0);
+      DenseGradArgs g;
+      g.blocks = (const DBlock*)DT->dblocks.p;
+      g.pblocks = (const int32_t*)DT->dpblocks.p;
+      g.gates = (const DGate*)DT->dgates.p;
+      g.fixed = (const double*)DT->fixed.p;
+      g.theta = theta;
+      g.P = P.P;
+      g.rs = (const double*)(W + wl.drs);
+      g.acc_total = P.dacc_total;
+      g.contrib = (double*)(W + wl.contrib);
+      g.ncontrib = std::max(P.n_contrib, 1);
+      g.b0 = b0;
+      dense_grad_kernel<<<dim3(npb, (unsigned)rows), 256, 0, st>>>(g);
+      CUDA_TRY(cudaGetLastError());
     }
   }
   // ---- finalize / export
@@ -1036,6 +1243,13 @@ tcx_status tcx_circuit_info(const tcx_circuit* circ, const tcx_pauli* pauli, tcx
   o->tiles_per_state = P.tiles;
   o->acc_slots = P.acc_total;
   o->mat_reals = P.mat_total;
+  o->dense_k = P.dense_k;
+  o->dense_blocks = (int)P.dblocks.size();
+  if (!P.dblocks.empty()) {  // the trailing E / lambda pass has no gates: no backward launch
+    int nb = 0;
+    for (auto& p : P.passes) nb += p.ops.empty() ? 0 : 1;
+    o->bwd_passes = nb;
+  }
   o->lambda_passes = 0;
   if (pauli) {
     std::shared_ptr<Binding> Bd;
@@ -1192,6 +1406,17 @@ tcx_status tcx_launch_count(const tcx_circuit* circ, const tcx_pauli* pauli, int
   const int64_t chunks = (B + 65534) / 65535;
   int64_t per = 0;
   per += P.mitems.empty() ? 0 : 1;
+  if (!P.dblocks.empty()) {
+    int npb = 0;
+    for (auto& d : P.dblocks) npb += d.has_param;
+    per += (P.dmat_shared > 0 ? 1 : 0) + (P.dmat_row > 0 ? 1 : 0) + (int64_t)P.dblocks.size();
+    if (want_grad) {
+      int nbw = 0;
+      for (size_t i = 0; i < P.dblocks.size(); ++i) nbw += (i > 0 || P.dblocks[i].has_param) ? 1 : 0;
+      per += nbw + npb + (npb > 0 ? 1 : 0);  // backward blocks, R' sums, contributions
+      for (auto& p : P.passes) per -= p.ops.empty() ? 1 : 0;  // no backward of the E pass
+    }
+  }
   if (wl.mega)
     per += 1;
   else

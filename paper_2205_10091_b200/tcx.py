@@ -45,7 +45,7 @@ class tcx_build_opts(ctypes.Structure):
     _fields_ = [("tile_bits", ctypes.c_int32), ("reg_bits", ctypes.c_int32),
                 ("coalesce_bits", ctypes.c_int32), ("max_ops_per_pass", ctypes.c_int32),
                 ("jit", ctypes.c_int32), ("global_bits", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 2)]
+                ("dense_k", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class tcx_plan_info(ctypes.Structure):
@@ -53,7 +53,8 @@ class tcx_plan_info(ctypes.Structure):
         "n_qubits", "n_params", "dtype", "tile_bits", "reg_bits", "coalesce_bits",
         "threads_per_tile", "n_ops", "fwd_passes", "lambda_passes", "bwd_passes", "stages",
         "unitary", "relabeled", "jit", "global_bits", "segments")] + [(f, ctypes.c_int64) for f in (
-            "tiles_per_state", "acc_slots", "mat_reals")]
+            "tiles_per_state", "acc_slots", "mat_reals")] + [(f, ctypes.c_int32) for f in (
+            "dense_k", "dense_blocks")]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -64,7 +65,8 @@ class tcx_kernel_time(ctypes.Structure):
                 ("pad", ctypes.c_float), ("flops", ctypes.c_double), ("bytes", ctypes.c_double)]
 
 
-PHASES = {0: "materialize", 1: "forward", 2: "lambda", 3: "backward", 4: "finalize", 5: "fused"}
+PHASES = {0: "materialize", 1: "forward", 2: "lambda", 3: "backward", 4: "finalize", 5: "fused",
+          6: "dense", 7: "dense_backward"}
 
 
 class tcx_shard_step(ctypes.Structure):
@@ -143,7 +145,7 @@ class Circuit:
 
     def __init__(self, circ, dtype: str = "c64", tile_bits: int = 0, reg_bits: int = 0,
                  coalesce_bits: int = 0, max_ops_per_pass: int = 0, jit: bool = True,
-                 global_bits: int = 0, gates=None):
+                 global_bits: int = 0, gates=None, dense_k: int = 0):
         names, q0, q1, param, coeff, moff, mats = circ.arrays()
         self.n = circ.n
         self.P = circ.n_params
@@ -155,7 +157,7 @@ class Circuit:
             mats = np.zeros(2)
         self._mats = mats
         opts = tcx_build_opts(tile_bits, reg_bits, coalesce_bits, max_ops_per_pass,
-                              0 if jit else -1, global_bits)
+                              0 if jit else -1, global_bits, dense_k)
         self.global_bits = global_bits
         h = _vp()
         _check(_lib.tcx_circuit_build(self.n, self.P, self._gates, self.G,

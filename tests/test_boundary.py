@@ -160,3 +160,21 @@ def test_bench_reference_arm_runs():
     line = json.loads(out.strip().splitlines()[-1])
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "oracle" and line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_dense_plan_blocks():
+    """Dense k-qubit fusion (tcx_build_opts.dense_k): block counts fall with k,
+    a single-qubit run is one block, 2-qubit gates force >= 2-qubit blocks, bad k errors."""
+    from paper_2205_10091_b200 import tcx as m
+    c = W.Circuit(3, 2).add("rx", 0, param=0, coeff=1.0).add("ry", 0, param=1, coeff=1.0).add("h", 0)
+    assert m.Circuit(c, "c64", dense_k=1).info()["dense_blocks"] == 1
+    c2 = W.random_deep_circuit(12, 10, 4)
+    counts = [m.Circuit(c2, "c128", dense_k=k).info()["dense_blocks"] for k in range(1, 6)]
+    assert all(a >= b for a, b in zip(counts, counts[1:])), counts
+    assert counts[0] > counts[-1]
+    # a brick layer of CZs alone: k = 1 still gives 2-qubit blocks (one per CZ pair run)
+    assert m.Circuit(W.hea(6, 1), "c64", dense_k=6 - 1).info()["dense_blocks"] >= 1
+    with pytest.raises(m.TcxError):
+        m.Circuit(c2, "c64", dense_k=6)
+    with pytest.raises(m.TcxError):
+        m.Circuit(W.hea(8, 1), "c64", dense_k=2, global_bits=1)

@@ -1,0 +1,122 @@
+"""GPU parity of the dense k-qubit block path (tcx_build_opts.dense_k) vs the
+CPU oracle.  Tolerances as tests/helpers.py."""
+import os
+
+import numpy as np
+import pytest
+
+import workloads as W
+from helpers import check_E, check_grad, state_tol
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tc():
+    import torch
+    from paper_2205_10091_b200 import tcx
+    assert torch.cuda.is_available()
+    return tcx
+
+
+def _th(theta):
+    import torch
+    return torch.as_tensor(np.ascontiguousarray(theta, dtype=np.float64)).cuda()
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("n", [2, 3, 6, 9, 13])
+def test_dense_state_random_all_kinds(tc, dtype, k, n):
+    """Every gate kind (fixed, rotations, payloads, SWAP relabels) fused into dense blocks;
+    n = 13 spans many CTAs and columns per row."""
+    c = W.random_circuit(n, 70, 5000 + 7 * n + k, n_params=5, with_payload=True)
+    th = W.thetas(3, 5, n + k)
+    C = tc.Circuit(c, dtype, dense_k=k)
+    info = C.info()
+    assert info["dense_k"] == k and info["dense_blocks"] >= 1
+    psi = tc.state_batch(C, _th(th)).cpu().numpy()
+    for b in range(3):
+        ref = orc.state(c, th[b])
+        err = np.abs(psi[b] - ref).max()
+        assert err <= state_tol(dtype, len(c.gates)), f"k={k} row {b}: {err}"
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
+def test_dense_expect(tc, dtype, k):
+    n = 12
+    c, H = W.hea(n, 3), W.heisenberg(n)
+    th = W.thetas(4, c.n_params, 11 + k)
+    C, P = tc.Circuit(c, dtype, dense_k=k), tc.Pauli(H)
+    E = tc.expect_batch(C, P, _th(th)).cpu().numpy()
+    Er = orc.expect_batch(c, H, th, nthreads=os.cpu_count() or 1)
+    check_E(E, Er, H, dtype, f"k={k}")
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
+@pytest.mark.parametrize("n,seed", [(3, 1), (7, 2), (11, 3), (15, 4)])
+def test_dense_grad_random(tc, dtype, k, n, seed):
+    """Adjoint through dense blocks: U^dagger on psi and lambda, R' = sum psi lam^dagger over
+    every column, grad_g = coeff_g Im Tr(S_g P_g S_g^dagger R')."""
+    c = W.random_circuit(n, 80, 6000 + 10 * n + k, n_params=7, with_payload=True)
+    H = W.random_pauli_sum(n, 10, 60 + seed)
+    th = W.thetas(3, 7, seed + k)
+    C, P = tc.Circuit(c, dtype, dense_k=k), tc.Pauli(H)
+    E, G = tc.grad_batch(C, P, _th(th))
+    Er, Gr = orc.value_grad_batch(c, H, th, nthreads=os.cpu_count() or 1)
+    check_E(E.cpu().numpy(), Er, H, dtype, f"k={k} E")
+    check_grad(G.cpu().numpy(), Gr, H, c, dtype, f"k={k} grad")
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("k", [2, 4])
+def test_dense_grad_hea_heisenberg(tc, dtype, k):
+    """cfg2-shaped (HEA + Heisenberg, shared-nothing parameters) at n = 14."""
+    n = 14
+    c, H = W.hea(n, 3), W.heisenberg(n)
+    th = W.thetas(3, c.n_params, 5)
+    C, P = tc.Circuit(c, dtype, dense_k=k), tc.Pauli(H)
+    E, G = tc.grad_batch(C, P, _th(th))
+    Er, Gr = orc.value_grad_batch(c, H, th, nthreads=os.cpu_count() or 1)
+    check_E(E.cpu().numpy(), Er, H, dtype)
+    check_grad(G.cpu().numpy(), Gr, H, c, dtype)
+
+
+def test_dense_grad_k5_unsupported(tc):
+    c, H = W.hea(6, 2), W.tfim_zz_x(6)
+    C, P = tc.Circuit(c, "c64", dense_k=5), tc.Pauli(H)
+    with pytest.raises(tc.TcxError):
+        tc.grad_batch(C, P, _th(W.thetas(1, c.n_params, 1)))
+
+
+@pytest.mark.parametrize("k", [1, 3, 5])
+def test_dense_random_deep_matches_window_path(tc, k):
+    """cfg4-shaped brick circuit (n = 16, 12 layers, complex128): dense blocks vs the
+    oracle state."""
+    c = W.random_deep_circuit(16, 12, 4)
+    C = tc.Circuit(c, "c128", dense_k=k)
+    psi = tc.state_batch(C, _th(np.zeros((1, 0)))).cpu().numpy()[0]
+    ref = orc.state(c, np.zeros(0))
+    assert np.abs(psi - ref).max() <= state_tol("c128", len(c.gates))
+
+
+def test_dense_roundtrip_u_udagger_30q(tc):
+    """Full cfg4 size (n = 30, complex128): U followed by U^dagger (the reversed, inverted
+    gate list) returns |0...0> through the dense k = 4 path; sampled amplitudes."""
+    import torch
+    c = W.random_deep_circuit(30, 6, 4)
+    inv = W.Circuit(30, 0)
+    for g in reversed(c.gates):
+        inv.gates.append(W.Gate(g.name, g.q0, g.q1, -1, -g.coeff if g.name in ("rx", "ry", "rz") else g.coeff))
+    full = W.Circuit(30, 0)
+    full.gates = list(c.gates) + list(inv.gates)
+    C = tc.Circuit(full, "c128", dense_k=4)
+    psi = tc.state_batch(C, _th(np.zeros((1, 0))))
+    assert abs(complex(psi[0, 0].item()) - 1.0) < 1e-11
+    idx = torch.randint(1, 1 << 30, (4096,), generator=torch.Generator().manual_seed(0)).cuda()
+    assert psi[0, idx].abs().max().item() < 1e-11
+    del psi
+    torch.cuda.empty_cache()
