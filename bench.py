@@ -156,6 +156,8 @@ def main():
     ap.add_argument("--coalesce-bits", type=int, default=0)
     ap.add_argument("--reg-bits", type=int, default=0)
     ap.add_argument("--max-ops-per-pass", type=int, default=0)
+    ap.add_argument("--dtype", default=None, choices=["c64", "c128"],
+                    help="override the config's state dtype (studies; e.g. cfg4 at complex64)")
     ap.add_argument("--dense-k", type=int, default=0,
                     help="fuse gates into dense k-qubit blocks (k = 1..5; cfg4 k-sweep)")
     ap.add_argument("--jit", type=int, default=1, help="1: per-circuit specialised kernels")
@@ -189,6 +191,8 @@ def main():
         return run_sharded(args, world, rank, local, dev)
 
     name, circ, H, theta, dtype = W.config(args.config, B=args.batch)
+    if args.dtype and args.dtype != dtype:
+        name, dtype = name.replace("_" + dtype, "_" + args.dtype), args.dtype
     B = theta.shape[0]
     if world > 1 and rank > 0:  # distinct seeded rows per rank (weak scaling)
         theta = W.thetas(B, circ.n_params, 1000 + rank) if args.config != 2 else \
@@ -344,7 +348,7 @@ def main():
                                                  "lambda_passes", "bwd_passes", "stages",
                                                  "n_ops", "jit", "dense_k", "dense_blocks")},
                    "jit_compile_s": round(t_jit, 2), "mode": mode,
-                   "max_ops_per_pass": args.max_ops_per_pass},
+                   "max_ops_per_pass": args.max_ops_per_pass, "dense_k": args.dense_k},
         "roofline": roof,
         "kernels": kernel_split,
         "cpu_baseline": cpu,

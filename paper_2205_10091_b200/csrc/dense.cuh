@@ -231,34 +231,45 @@ __global__ void __launch_bounds__(256) dense_fwd_kernel(const DenseArgs a) {
           if (ok[u]) v[u][j] = psi[base[u] | dense_off<K>(j, bits)];
       }
     }
+    // IR output rows at a time: 2 * IR * COLS independent accumulation chains per thread
+    constexpr int IR = D < 4 ? D : 4;
 #pragma unroll
-    for (int i = 0; i < D; ++i) {
-      C acc[COLS];
+    for (int i0 = 0; i0 < D; i0 += IR) {
+      C acc[IR][COLS];
 #pragma unroll
-      for (int u = 0; u < COLS; ++u) acc[u] = C{Real(0), Real(0)};
+      for (int r = 0; r < IR; ++r)
+#pragma unroll
+        for (int u = 0; u < COLS; ++u) acc[r][u] = C{Real(0), Real(0)};
 #pragma unroll
       for (int j = 0; j < D; ++j) {
-        if (kF) {
-          const q64 ur = reinterpret_cast<const q64*>(sU)[2 * (i * D + j)];
-          const q64 ui = reinterpret_cast<const q64*>(sU)[2 * (i * D + j) + 1];
 #pragma unroll
-          for (int u = 0; u < COLS; ++u) {
-            const q64 vv = f2u_(*reinterpret_cast<const Cx<float>*>(&v[u][j]));
-            q64 ac = f2u_(*reinterpret_cast<const Cx<float>*>(&acc[u]));
-            ac = qfma(ur, vv, ac);
-            ac = qfma(ui, qsw(vv), ac);
-            *reinterpret_cast<Cx<float>*>(&acc[u]) = u2f_(ac);
+        for (int r = 0; r < IR; ++r) {
+          const int i = i0 + r;
+          if (kF) {
+            const q64 ur = reinterpret_cast<const q64*>(sU)[2 * (i * D + j)];
+            const q64 ui = reinterpret_cast<const q64*>(sU)[2 * (i * D + j) + 1];
+#pragma unroll
+            for (int u = 0; u < COLS; ++u) {
+              const q64 vv = f2u_(*reinterpret_cast<const Cx<float>*>(&v[u][j]));
+              q64 ac = f2u_(*reinterpret_cast<const Cx<float>*>(&acc[r][u]));
+              ac = qfma(ur, vv, ac);
+              ac = qfma(ui, qsw(vv), ac);
+              *reinterpret_cast<Cx<float>*>(&acc[r][u]) = u2f_(ac);
+            }
+          } else {
+            const Cx<double> uu{sU[2 * (i * D + j)], sU[2 * (i * D + j) + 1]};
+#pragma unroll
+            for (int u = 0; u < COLS; ++u)
+              cmac(*reinterpret_cast<Cx<double>*>(&acc[r][u]), uu,
+                   *reinterpret_cast<const Cx<double>*>(&v[u][j]));
           }
-        } else {
-          const Cx<double> uu{sU[2 * (i * D + j)], sU[2 * (i * D + j) + 1]};
-#pragma unroll
-          for (int u = 0; u < COLS; ++u)
-            cmac(*reinterpret_cast<Cx<double>*>(&acc[u]), uu, *reinterpret_cast<const Cx<double>*>(&v[u][j]));
         }
       }
 #pragma unroll
-      for (int u = 0; u < COLS; ++u)
-        if (ok[u]) psi[base[u] | dense_off<K>(i, bits)] = acc[u];
+      for (int r = 0; r < IR; ++r)
+#pragma unroll
+        for (int u = 0; u < COLS; ++u)
+          if (ok[u]) psi[base[u] | dense_off<K>(i0 + r, bits)] = acc[r][u];
     }
   }
 }
@@ -355,19 +366,28 @@ __global__ void __launch_bounds__(256) dense_bwd_kernel(const DenseArgs a) {
       }
     }
     if (a.store && ok) {
+      constexpr int IR = D < 4 ? D : 4;  // independent accumulation chains
 #pragma unroll
-      for (int i = 0; i < D; ++i) {
-        C pv{Real(0), Real(0)}, pl{Real(0), Real(0)};
+      for (int i0 = 0; i0 < D; i0 += IR) {
+        C pv[IR], pl[IR];
+#pragma unroll
+        for (int r = 0; r < IR; ++r) pv[r] = pl[r] = C{Real(0), Real(0)};
 #pragma unroll
         for (int j = 0; j < D; ++j) {
-          const C u = sU[j * D + i];  // conj(U_ji)
-          pv.x = fma(u.x, v[j].x, fma(u.y, v[j].y, pv.x));
-          pv.y = fma(u.x, v[j].y, fma(-u.y, v[j].x, pv.y));
-          pl.x = fma(u.x, l[j].x, fma(u.y, l[j].y, pl.x));
-          pl.y = fma(u.x, l[j].y, fma(-u.y, l[j].x, pl.y));
+#pragma unroll
+          for (int r = 0; r < IR; ++r) {
+            const C u = sU[j * D + i0 + r];  // conj(U_ji)
+            pv[r].x = fma(u.x, v[j].x, fma(u.y, v[j].y, pv[r].x));
+            pv[r].y = fma(u.x, v[j].y, fma(-u.y, v[j].x, pv[r].y));
+            pl[r].x = fma(u.x, l[j].x, fma(u.y, l[j].y, pl[r].x));
+            pl[r].y = fma(u.x, l[j].y, fma(-u.y, l[j].x, pl[r].y));
+          }
         }
-        psi[base | dense_off<K>(i, bits)] = pv;
-        lam[base | dense_off<K>(i, bits)] = pl;
+#pragma unroll
+        for (int r = 0; r < IR; ++r) {
+          psi[base | dense_off<K>(i0 + r, bits)] = pv[r];
+          lam[base | dense_off<K>(i0 + r, bits)] = pl[r];
+        }
       }
     }
   }

@@ -21,6 +21,7 @@
 #include "jit.h"
 #include "kernels.cuh"
 #include "dense.cuh"
+#include "dense_tc.cuh"
 #include "plan.h"
 
 using namespace tcx;
@@ -573,8 +574,30 @@ void dense_fwd_launch(DenseArgs& a, int64_t rows, cudaStream_t st) {
   const int64_t gx = std::max<int64_t>(1, std::min<int64_t>(need, std::max<int64_t>(1, 148 * 8 / rows)));
   dense_fwd_kernel<Real, K, COLS><<<dim3((unsigned)gx, (unsigned)rows), 256, 0, st>>>(a);
 }
+// complex64 k >= 4 blocks on tcgen05 (dense_tc.cuh); TCX_DENSE_TC=0 keeps them on FP32 FMA
+bool dense_tc_on(int K) {
+  static const int mode = [] {
+    const char* e = getenv("TCX_DENSE_TC");
+    return e ? atoi(e) : 1;
+  }();
+  return mode != 0 && K == 5;
+}
+template <int K>
+cudaError_t dense_fwd_tc_launch(DenseArgs& a, int64_t rows, cudaStream_t st) {
+  const int sm = dense_tc_smem(K);
+  cudaError_t e = cudaFuncSetAttribute(dense_fwd_tc_kernel<K>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  if (e != cudaSuccess) return e;
+  const int64_t ncols = ((int64_t)1 << a.n) >> K;
+  const int64_t tiles = (ncols + 127) / 128;
+  const int64_t gx = std::max<int64_t>(1, std::min<int64_t>(tiles, std::max<int64_t>(1, 148 * 2 / rows)));
+  dense_fwd_tc_kernel<K><<<dim3((unsigned)gx, (unsigned)rows), 128, sm, st>>>(a);
+  return cudaGetLastError();
+}
 template <typename Real>
 cudaError_t dense_fwd(int K, DenseArgs& a, int64_t rows, cudaStream_t st) {
+  if (sizeof(Real) == 4 && dense_tc_on(K))
+    return K == 5 ? dense_fwd_tc_launch<5>(a, rows, st) : dense_fwd_tc_launch<4>(a, rows, st);
   switch (K) {
     case 1: dense_fwd_launch<Real, 1>(a, rows, st); break;
     case 2: dense_fwd_launch<Real, 2>(a, rows, st); break;

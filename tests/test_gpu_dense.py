@@ -120,3 +120,16 @@ def test_dense_roundtrip_u_udagger_30q(tc):
     assert psi[0, idx].abs().max().item() < 1e-11
     del psi
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("n,B", [(14, 3), (22, 1)])
+def test_dense_k5_c64_tensor_core_multi_tile(tc, n, B):
+    """complex64 k = 5 blocks run on tcgen05 (3xTF32, dense_tc.cuh): several 128-column tiles
+    per CTA (n = 22, B = 1) and several rows (n = 14); checked against the oracle state."""
+    c = W.random_deep_circuit(n, 4, 9 + n)
+    c.n_params = 0
+    C = tc.Circuit(c, "c64", dense_k=5)
+    psi = tc.state_batch(C, _th(np.zeros((B, 0)))).cpu().numpy()
+    ref = orc.state(c, np.zeros(0))
+    for b in range(B):
+        assert np.abs(psi[b] - ref).max() <= state_tol("c64", len(c.gates))

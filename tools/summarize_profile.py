@@ -24,7 +24,10 @@ def read_csv(path):
 
 
 def kclass(name):
-    for k, c in (("tcx_jit_bwd", "backward"), ("tcx_jit_fwd", "forward"), ("tcx_jit_mega", "fused"),
+    for k, c in (("dense_fwd_tc", "dense (tcgen05)"), ("dense_fwd", "dense"),
+                 ("dense_bwd", "dense_backward"), ("dense_mat", "materialize"),
+                 ("dense_grad", "finalize"), ("dense_rsum", "finalize"),
+                 ("tcx_jit_bwd", "backward"), ("tcx_jit_fwd", "forward"), ("tcx_jit_mega", "fused"),
                  ("pass_kernel", "pass_kernel (generic)"), ("materialize", "materialize"),
                  ("finalize", "finalize")):
         if k in name:
@@ -43,7 +46,9 @@ def main():
             per[(int(r["ID"]), r["Kernel Name"])] = float(r["Metric Value"])
     ids = sorted(per)
     # one step = launches after the last materialize kernel
-    last_mat = max(i for i, (k, n) in enumerate(ids) if "materialize" in n)
+    firsts = [i for i, (k, n) in enumerate(ids) if "materialize" in n or "dense_mat" in n]
+    # a step starts at its first materialize launch (dense plans may launch two)
+    last_mat = max(i for i in firsts if i == 0 or i - 1 not in firsts) if firsts else 0
     step = ids[last_mat:]
     tot = sum(per[k] for k in step)
     by = defaultdict(float)
@@ -76,10 +81,10 @@ def main():
         lines.append(f"| {c} | {len(v)} | {sum(v) / len(v) / 1e9:.3f} |")
         traffic[c] = sum(v) / len(v)
     # full captures
-    for kind in ("bwd", "fwd"):
-        rep = os.path.join(OUT, f"prof_{kind}_{tag}.ncu-rep")
-        if not os.path.exists(rep):
-            continue
+    import glob
+    reps = sorted(glob.glob(os.path.join(OUT, f"prof_*_{tag}.ncu-rep")))
+    for rep in reps:
+        kind = os.path.basename(rep)[len("prof_"):-len(f"_{tag}.ncu-rep")]
         raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                              text=True).stdout
         rows = list(csv.reader(io.StringIO(raw)))
@@ -95,8 +100,12 @@ def main():
                 "dram__throughput.avg.pct_of_peak_sustained_elapsed",
                 "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active",
                 "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
-                "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum"]
-        lines += ["", f"## `ncu --set full` capture: {kind} pass kernel", "", "| metric | value |", "|---|---|"]
+                "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum",
+                "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+                "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active",
+                "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+                "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"]
+        lines += ["", f"## `ncu --set full` capture: {kind} kernel", "", "| metric | value |", "|---|---|"]
         for k in keys:
             if k in d:
                 lines.append(f"| {k} | {d[k]} {u.get(k, '')} |")
