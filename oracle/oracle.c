@@ -211,16 +211,22 @@ static double angle_of(int g, const int *param, const double *coeff, const doubl
 }
 
 /* ------------------------------------------------------------- state() */
-/* psi = U_G ... U_1 |0..0>; gate `shift_gate` gets its angle shifted by `shift`
- * (used only by the parameter-shift gradient).  out: 2^n interleaved (re, im). */
+/* psi = U_G ... U_1 |psi0>, psi0 = |0..0> when NULL (PAPER.md:391 default input) or
+ * the caller's input state ("inputs" batched with the parameters,
+ * SURVEY §8f f2); gate `shift_gate` gets its angle shifted by `shift` (used only by the
+ * parameter-shift gradient).  out: 2^n interleaved (re, im). */
 static void state_c(int n, int G, const int *kind, const int *q0, const int *q1,
                     const int *param, const double *coeff, const int64_t *moff,
                     const double *mats, const double *theta, int shift_gate, double shift,
-                    cplx *psi)
+                    cplx *psi, const cplx *psi0)
 {
     const int64_t N = (int64_t)1 << n;
-    for (int64_t r = 0; r < N; ++r) psi[r] = 0;
-    psi[0] = 1;                                   /* PAPER.md:391 default input */
+    if (psi0) {
+        memcpy(psi, psi0, sizeof(cplx) * N);
+    } else {
+        for (int64_t r = 0; r < N; ++r) psi[r] = 0;
+        psi[0] = 1;                               /* PAPER.md:391 default input */
+    }
     for (int g = 0; g < G; ++g) {
         cplx m[16];
         double a = angle_of(g, param, coeff, theta, shift_gate, shift);
@@ -233,7 +239,16 @@ int orc_state(int n, int G, const int *kind, const int *q0, const int *q1,
               const int *param, const double *coeff, const int64_t *moff,
               const double *mats, const double *theta, double *out)
 {
-    state_c(n, G, kind, q0, q1, param, coeff, moff, mats, theta, -1, 0.0, (cplx *)out);
+    state_c(n, G, kind, q0, q1, param, coeff, moff, mats, theta, -1, 0.0, (cplx *)out, NULL);
+    return 0;
+}
+
+int orc_state_in(int n, int G, const int *kind, const int *q0, const int *q1,
+                 const int *param, const double *coeff, const int64_t *moff,
+                 const double *mats, const double *theta, const double *psi0, double *out)
+{
+    state_c(n, G, kind, q0, q1, param, coeff, moff, mats, theta, -1, 0.0, (cplx *)out,
+            (const cplx *)psi0);
     return 0;
 }
 
@@ -290,7 +305,7 @@ static double energy(int n, int G, const int *kind, const int *q0, const int *q1
                      int T, const unsigned char *codes, const double *w, cplx *psi)
 {
     double e[2];
-    state_c(n, G, kind, q0, q1, param, coeff, moff, mats, theta, shift_gate, shift, psi);
+    state_c(n, G, kind, q0, q1, param, coeff, moff, mats, theta, shift_gate, shift, psi, NULL);
     orc_expect(n, (const double *)psi, T, codes, w, e);
     return e[0];
 }
@@ -301,17 +316,17 @@ static double energy(int n, int G, const int *kind, const int *q0, const int *q1
  *   psi <- U_g^dag psi; lambda <- U_g^dag lambda.
  * (d/da <psi|H|psi> with U = exp(-i a P/2) gives 2 Re <lambda|(-i/2) P|psi> = Im<lambda|P|psi>.)
  * E[0] = Re <psi|H|psi>, E[1] = Im (must be ~0). */
-int orc_value_grad(int n, int G, const int *kind, const int *q0, const int *q1,
-                   const int *param, const double *coeff, const int64_t *moff,
-                   const double *mats, int P, const double *theta,
-                   int T, const unsigned char *codes, const double *w,
-                   double *E, double *grad)
+static int value_grad_c(int n, int G, const int *kind, const int *q0, const int *q1,
+                        const int *param, const double *coeff, const int64_t *moff,
+                        const double *mats, int P, const double *theta,
+                        int T, const unsigned char *codes, const double *w,
+                        double *E, double *grad, const cplx *psi0)
 {
     const int64_t N = (int64_t)1 << n;
     cplx *psi = malloc(sizeof(cplx) * N), *lam = malloc(sizeof(cplx) * N);
     cplx *tmp = malloc(sizeof(cplx) * N);
     if (!psi || !lam || !tmp) { free(psi); free(lam); free(tmp); return -2; }
-    state_c(n, G, kind, q0, q1, param, coeff, moff, mats, theta, -1, 0.0, psi);
+    state_c(n, G, kind, q0, q1, param, coeff, moff, mats, theta, -1, 0.0, psi, psi0);
     hamiltonian_apply(n, T, codes, w, psi, lam, tmp);
     cplx e = inner(N, psi, lam);
     E[0] = creal(e);
@@ -334,6 +349,16 @@ int orc_value_grad(int n, int G, const int *kind, const int *q0, const int *q1,
     }
     free(psi); free(lam); free(tmp);
     return 0;
+}
+
+int orc_value_grad(int n, int G, const int *kind, const int *q0, const int *q1,
+                   const int *param, const double *coeff, const int64_t *moff,
+                   const double *mats, int P, const double *theta,
+                   int T, const unsigned char *codes, const double *w,
+                   double *E, double *grad)
+{
+    return value_grad_c(n, G, kind, q0, q1, param, coeff, moff, mats, P, theta, T, codes, w,
+                        E, grad, NULL);
 }
 
 /* ---------------------------------------------------- parameter shift */
@@ -365,22 +390,45 @@ int orc_param_shift(int n, int G, const int *kind, const int *q0, const int *q1,
 /* Rows are independent (PAPER.md:1121-1139 batched VQE; grad per row).
  * nthreads > 1 runs rows in parallel with OpenMP (used only for the reported CPU
  * baseline); the arithmetic per row is identical. */
+/* psi0: NULL (all rows start from |0..0>) or [B][2^n] interleaved input states */
+static int value_grad_batch_c(int n, int G, const int *kind, const int *q0, const int *q1,
+                              const int *param, const double *coeff, const int64_t *moff,
+                              const double *mats, int P, int B, const double *theta,
+                              int T, const unsigned char *codes, const double *w,
+                              double *E, double *grad, int nthreads, const double *psi0)
+{
+    int err = 0;
+    const int64_t N = (int64_t)1 << n;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads > 0 ? nthreads : 1) reduction(|:err)
+#endif
+    for (int b = 0; b < B; ++b)
+        err |= value_grad_c(n, G, kind, q0, q1, param, coeff, moff, mats, P,
+                            theta + (int64_t)b * P, T, codes, w, E + 2 * b,
+                            grad + (int64_t)b * P,
+                            psi0 ? (const cplx *)(psi0 + 2 * N * b) : NULL) != 0;
+    (void)nthreads;
+    return err ? -2 : 0;
+}
+
 int orc_value_grad_batch(int n, int G, const int *kind, const int *q0, const int *q1,
                          const int *param, const double *coeff, const int64_t *moff,
                          const double *mats, int P, int B, const double *theta,
                          int T, const unsigned char *codes, const double *w,
                          double *E /* [B][2] */, double *grad /* [B][P] */, int nthreads)
 {
-    int err = 0;
-#ifdef _OPENMP
-#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads > 0 ? nthreads : 1) reduction(|:err)
-#endif
-    for (int b = 0; b < B; ++b)
-        err |= orc_value_grad(n, G, kind, q0, q1, param, coeff, moff, mats, P,
-                              theta + (int64_t)b * P, T, codes, w, E + 2 * b,
-                              grad + (int64_t)b * P) != 0;
-    (void)nthreads;
-    return err ? -2 : 0;
+    return value_grad_batch_c(n, G, kind, q0, q1, param, coeff, moff, mats, P, B, theta, T,
+                              codes, w, E, grad, nthreads, NULL);
+}
+
+int orc_value_grad_batch_in(int n, int G, const int *kind, const int *q0, const int *q1,
+                            const int *param, const double *coeff, const int64_t *moff,
+                            const double *mats, int P, int B, const double *theta,
+                            int T, const unsigned char *codes, const double *w,
+                            double *E, double *grad, int nthreads, const double *psi0)
+{
+    return value_grad_batch_c(n, G, kind, q0, q1, param, coeff, moff, mats, P, B, theta, T,
+                              codes, w, E, grad, nthreads, psi0);
 }
 
 int orc_expect_batch(int n, int G, const int *kind, const int *q0, const int *q1,
@@ -398,7 +446,7 @@ int orc_expect_batch(int n, int G, const int *kind, const int *q0, const int *q1
         cplx *psi = malloc(sizeof(cplx) * N);
         if (!psi) { err |= 1; continue; }
         state_c(n, G, kind, q0, q1, param, coeff, moff, mats, theta + (int64_t)b * P,
-                -1, 0.0, psi);
+                -1, 0.0, psi, NULL);
         err |= orc_expect(n, (const double *)psi, T, codes, w, E + 2 * b) != 0;
         free(psi);
     }

@@ -98,6 +98,21 @@ def state(circ, theta) -> np.ndarray:
     return out.view(np.complex128)
 
 
+def state_in(circ, theta, psi0) -> np.ndarray:
+    """U(theta) psi0 for a caller-given input state psi0 [2^n] (PAPER.md:1005-1044 inputs)."""
+    g = _Gates(circ)
+    th = np.ascontiguousarray(np.asarray(theta, dtype=np.float64).reshape(-1))
+    if th.size == 0:
+        th = np.zeros(1)
+    p0 = np.ascontiguousarray(np.asarray(psi0, dtype=np.complex128).reshape(-1))
+    assert p0.size == 1 << circ.n
+    out = np.zeros(2 << circ.n, dtype=np.float64)
+    rc = lib().orc_state_in(*g.args, _p(th, ctypes.c_double), _p(p0.view(np.float64), ctypes.c_double),
+                            _p(out, ctypes.c_double))
+    assert rc == 0
+    return out.view(np.complex128)
+
+
 def expect_state(n, psi, H):
     """(Re, Im) of sum_j alpha_j <psi|P_j|psi>."""
     psi = np.ascontiguousarray(psi, dtype=np.complex128)
@@ -155,6 +170,27 @@ def value_grad_batch(circ, H, theta, nthreads: int = 1):
                                     _p(codes, ctypes.c_ubyte), _p(w, ctypes.c_double),
                                     _p(E, ctypes.c_double), _p(grad, ctypes.c_double),
                                     ctypes.c_int(nthreads))
+    assert rc == 0
+    return E[:, 0], grad[:, :P]
+
+
+def value_grad_batch_in(circ, H, theta, psi0, nthreads: int = 1):
+    """E [B], grad [B, P] with row b starting from the input state psi0[b] (not |0...0>)."""
+    g = _Gates(circ)
+    th = np.ascontiguousarray(np.asarray(theta, dtype=np.float64))
+    B = th.shape[0]
+    P = circ.n_params
+    codes, w = _ham(H)
+    p0 = np.ascontiguousarray(np.asarray(psi0, dtype=np.complex128).reshape(B, 1 << circ.n))
+    E = np.zeros((B, 2))
+    grad = np.zeros((B, max(P, 1)))
+    if th.size == 0:
+        th = np.zeros((B, 1))
+    rc = lib().orc_value_grad_batch_in(*g.args, ctypes.c_int(P), ctypes.c_int(B),
+                                       _p(th, ctypes.c_double), ctypes.c_int(len(w)),
+                                       _p(codes, ctypes.c_ubyte), _p(w, ctypes.c_double),
+                                       _p(E, ctypes.c_double), _p(grad, ctypes.c_double),
+                                       ctypes.c_int(nthreads), _p(p0.view(np.float64), ctypes.c_double))
     assert rc == 0
     return E[:, 0], grad[:, :P]
 

@@ -343,3 +343,46 @@ def test_validation_rejects():
     assert orc.validate(c) == 2
     c = W.Circuit(3, 2).add("rx", 1, param=2, coeff=1.0)
     assert orc.validate(c) == 1
+
+
+# ---------------------------------------------------- input states
+def test_input_state_ghz_ry_closed_form():
+    """inputs= (a batch of input states vmapped with the parameters):
+    a hand-written GHZ input (|0..0> + |1..1>)/sqrt2, then Ry(t_i) on every qubit, on
+    TFIM(ZZ+X): E = sum cos t_i cos t_{i+1}, dE/dt_i = -sin t_i (cos t_{i-1} + cos t_{i+1})."""
+    n = 6
+    c = W.Circuit(n, n)
+    for q in range(n):
+        c.add("ry", q, param=q, coeff=1.0)
+    psi0 = np.zeros(1 << n, complex)
+    psi0[0] = psi0[-1] = 1 / np.sqrt(2)
+    th = np.random.default_rng(3).normal(size=(2, n))
+    E, G = orc.value_grad_batch_in(c, W.tfim_zz_x(n), th, np.stack([psi0, psi0]))
+    for b in range(2):
+        t = th[b]
+        Ec = sum(np.cos(t[i]) * np.cos(t[i + 1]) for i in range(n - 1))
+        Gc = np.array([-np.sin(t[i]) * ((np.cos(t[i - 1]) if i > 0 else 0) +
+                                        (np.cos(t[i + 1]) if i < n - 1 else 0)) for i in range(n)])
+        assert abs(E[b] - Ec) < 1e-12
+        np.testing.assert_allclose(G[b], Gc, atol=1e-12)
+
+
+def test_input_state_composition():
+    """U2 applied to the input U1|0> equals the concatenated circuit (state, E and the
+    gradient w.r.t. U2's parameters; U1 has fixed angles only)."""
+    n = 5
+    c1 = W.random_circuit(n, 30, 71, n_params=1)
+    for g in c1.gates:  # freeze U1
+        g.param = -1
+    c2 = W.random_circuit(n, 40, 72, n_params=6)
+    both = W.Circuit(n, 6)
+    both.gates = list(c1.gates) + list(c2.gates)
+    th = W.thetas(3, 6, 9)
+    p0 = orc.state(c1, np.zeros(1))
+    for b in range(3):
+        np.testing.assert_allclose(orc.state_in(c2, th[b], p0), orc.state(both, th[b]), atol=1e-13)
+    H = W.random_pauli_sum(n, 8, 5)
+    E, G = orc.value_grad_batch_in(c2, H, th, np.stack([p0] * 3))
+    Er, Gr = orc.value_grad_batch(both, H, th)
+    np.testing.assert_allclose(E, Er, atol=1e-12)
+    np.testing.assert_allclose(G, Gr, atol=1e-12)
