@@ -144,11 +144,12 @@ tcx_status tcx_circuit_build(int32_t n_qubits, int32_t n_params,
 tcx_status tcx_pauli_build(int32_t n_qubits, int32_t n_terms, const uint8_t* codes,
                            const double* weights, tcx_pauli** out);
 
-enum { TCX_WS_GRAD = 1, TCX_WS_HOST_IO = 2, TCX_WS_STATE = 4 };
+enum { TCX_WS_GRAD = 1, TCX_WS_HOST_IO = 2, TCX_WS_STATE = 4, TCX_WS_INPUTS = 8 };
 
 /* Device workspace bytes for a batch of B rows.  mode: TCX_WS_GRAD for tcx_grad_batch
  * (psi and lambda), 0 for tcx_expect_batch, TCX_WS_STATE for tcx_state_batch; OR
- * TCX_WS_HOST_IO for the *_host entries (adds device room for theta/E/grad). */
+ * TCX_WS_HOST_IO for the *_host entries (adds device room for theta/E/grad), and
+ * TCX_WS_INPUTS for the *_in entries (input states). */
 tcx_status tcx_workspace_bytes(const tcx_circuit* circ, const tcx_pauli* pauli, int64_t B,
                                int32_t mode, size_t* bytes);
 
@@ -170,6 +171,23 @@ tcx_status tcx_grad_batch(const tcx_circuit* circ, const tcx_pauli* pauli,
  * paper index order (qubit 0 most significant), for parity tests. */
 tcx_status tcx_state_batch(const tcx_circuit* circ, const double* theta, int64_t B,
                            void* state, void* ws, size_t ws_bytes, void* cuda_stream);
+
+/* Batched input states (`inputs` vmapped together with the weights,
+ * SURVEY §8f f2).  As tcx_expect_batch / tcx_grad_batch / tcx_state_batch, but row b
+ * starts from psi0[b] instead of |0...0>.  psi0: device [B][2^n] complex in the circuit
+ * dtype (complex64 / complex128, interleaved re, im), paper index order (qubit 0 most
+ * significant); read only, caller-owned; need not be normalised (E is then
+ * <psi|H|psi> of the unnormalised state).  ws sized with TCX_WS_INPUTS (| TCX_WS_GRAD /
+ * TCX_WS_STATE).  TCX_E_INVALID on a null psi0, TCX_E_UNSUPPORTED for sharded circuits. */
+tcx_status tcx_expect_batch_in(const tcx_circuit* circ, const tcx_pauli* pauli,
+                               const double* theta, int64_t B, const void* psi0, double* E,
+                               void* ws, size_t ws_bytes, void* cuda_stream);
+tcx_status tcx_grad_batch_in(const tcx_circuit* circ, const tcx_pauli* pauli,
+                             const double* theta, int64_t B, const void* psi0, double* E,
+                             double* grad, void* ws, size_t ws_bytes, void* cuda_stream);
+tcx_status tcx_state_batch_in(const tcx_circuit* circ, const double* theta, int64_t B,
+                              const void* psi0, void* state, void* ws, size_t ws_bytes,
+                              void* cuda_stream);
 
 /* End-to-end variants: theta/E/grad are HOST pointers (pinned memory recommended);
  * the call copies theta host->device, runs the same kernels, copies E/grad back and

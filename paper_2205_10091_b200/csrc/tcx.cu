@@ -494,14 +494,15 @@ int dense_max_k(const Plan& P) {
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-WsLayout ws_layout(const Plan& P, const Binding* Bd, int64_t B, int kind, bool host_io) {
+WsLayout ws_layout(const Plan& P, const Binding* Bd, int64_t B, int kind, bool host_io,
+                   bool inputs = false) {
   WsLayout w{};
   const size_t rs = P.dtype == TCX_C128 ? 8 : 4;
   const size_t N = size_t(1) << P.nloc;  // this rank's amplitudes (= 2^n unless sharded)
   const int64_t S = P.tiles / tiles_per_cta(P);
   const int EU = Bd ? (int)Bd->units.size() : 1;
   w.mega = kind != K_STATE && P.passes.size() == 1 && EU == 1 && P.gbits == 0 &&
-           P.dblocks.empty();
+           P.dblocks.empty() && !inputs;
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
@@ -639,7 +640,7 @@ struct OneStep {
 
 tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, double* E,
                double* grad, void* state, void* ws, size_t ws_bytes, cudaStream_t st, int kind,
-               const WsLayout* wl_in, const OneStep* one = nullptr) {
+               const WsLayout* wl_in, const OneStep* one = nullptr, const void* psi0 = nullptr) {
   if (P.gbits > 0 && !one)
     return fail(TCX_E_INVALID, "sharded circuit (global_bits > 0): use tcx_shard_program/exec");
   auto want = [&](int k, int a) { return !one || (one->kind == k && one->arg == a); };
@@ -667,7 +668,8 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
     if (H->p.n != P.n) return fail(TCX_E_INVALID, "pauli n_qubits != circuit n_qubits");
     if ((s = binding_for(P, H, Bd, &bdv))) return s;
   }
-  WsLayout wl = wl_in ? *wl_in : ws_layout(P, Bd.get(), B, kind, false);
+  if (psi0 && P.gbits > 0) return fail(TCX_E_UNSUPPORTED, "input states with a sharded state");
+  WsLayout wl = wl_in ? *wl_in : ws_layout(P, Bd.get(), B, kind, false, psi0 != nullptr);
   if (ws_bytes < wl.total)
     return fail(TCX_E_INVALID, "workspace too small: need " + std::to_string(wl.total) +
                                    " bytes, got " + std::to_string(ws_bytes));
@@ -697,6 +699,12 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
     else
       materialize_kernel<float><<<g, 128, 0, st>>>(ma);
     CUDA_TRY(cudaGetLastError());
+  }
+  // ---- input states (PAPER.md:1005-1044 inputs): the first pass / block reads them
+  if (psi0) {
+    if (wl.mega) return fail(TCX_E_INVALID, "workspace sized without TCX_WS_INPUTS");
+    CUDA_TRY(cudaMemcpyAsync(W + wl.psi, psi0, (size_t)B * ((size_t)1 << P.n) * 2 * rs,
+                             cudaMemcpyDeviceToDevice, st));
   }
   // ---- dense block matrices: row-independent blocks once, parameterised ones per row
   const bool dense = !P.dblocks.empty();
@@ -900,7 +908,7 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
         const int64_t rows = std::min(kMaxRows, B - b0);
         DenseArgs d;
         dense_args(d, blk);
-        d.init = di == 0 ? 1 : 0;
+        d.init = (di == 0 && !psi0) ? 1 : 0;
         d.b0 = b0;
         cudaError_t e = c128 ? dense_fwd<double>(blk.k, d, rows, st) : dense_fwd<float>(blk.k, d, rows, st);
         if (e != cudaSuccess) return fail(TCX_E_CUDA, std::string("dense block launch: ") + cudaGetErrorString(e));
@@ -919,7 +927,7 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
       const PassInfo& p = P.passes[pi];
       const bool last = pi == nP - 1 && !sharded;  // sharded: every lambda unit is its own step
       if (dense && kind == K_STATE && p.ops.empty()) continue;  // trailing pass: nothing to do
-      int mode = M_FWD | M_STORE_PSI | ((pi == 0 && !dense) ? M_INIT : M_LOAD_PSI);
+      int mode = M_FWD | M_STORE_PSI | ((pi == 0 && !dense && !psi0) ? M_INIT : M_LOAD_PSI);
       PassArgs a;
       base_args(a, p.wmask, p.W, mode);
       set_pass(a, p, true);
@@ -1153,7 +1161,8 @@ tcx_status tcx_workspace_bytes(const tcx_circuit* circ, const tcx_pauli* pauli, 
     tcx_status s = binding_for(P, pauli, Bd, nullptr);
     if (s) return s;
   }
-  *bytes = ws_layout(P, Bd.get(), B, kind, (mode & TCX_WS_HOST_IO) != 0).total;
+  *bytes = ws_layout(P, Bd.get(), B, kind, (mode & TCX_WS_HOST_IO) != 0,
+                     (mode & TCX_WS_INPUTS) != 0).total;
   return TCX_OK;
 }
 
@@ -1180,6 +1189,33 @@ tcx_status tcx_state_batch(const tcx_circuit* circ, const double* theta, int64_t
   if (!circ) return fail(TCX_E_INVALID, "null circuit");
   return run(const_cast<tcx_circuit*>(circ)->plan, nullptr, theta, B, nullptr, nullptr, state,
              ws, ws_bytes, (cudaStream_t)stream, K_STATE, nullptr);
+}
+
+tcx_status tcx_expect_batch_in(const tcx_circuit* circ, const tcx_pauli* pauli,
+                               const double* theta, int64_t B, const void* psi0, double* E,
+                               void* ws, size_t ws_bytes, void* stream) {
+  g_err.clear();
+  if (!circ || !psi0) return fail(TCX_E_INVALID, "null circuit or input states");
+  return run(const_cast<tcx_circuit*>(circ)->plan, pauli, theta, B, E, nullptr, nullptr, ws,
+             ws_bytes, (cudaStream_t)stream, K_EXPECT, nullptr, nullptr, psi0);
+}
+
+tcx_status tcx_grad_batch_in(const tcx_circuit* circ, const tcx_pauli* pauli,
+                             const double* theta, int64_t B, const void* psi0, double* E,
+                             double* grad, void* ws, size_t ws_bytes, void* stream) {
+  g_err.clear();
+  if (!circ || !psi0) return fail(TCX_E_INVALID, "null circuit or input states");
+  return run(const_cast<tcx_circuit*>(circ)->plan, pauli, theta, B, E, grad, nullptr, ws,
+             ws_bytes, (cudaStream_t)stream, K_GRAD, nullptr, nullptr, psi0);
+}
+
+tcx_status tcx_state_batch_in(const tcx_circuit* circ, const double* theta, int64_t B,
+                              const void* psi0, void* state, void* ws, size_t ws_bytes,
+                              void* stream) {
+  g_err.clear();
+  if (!circ || !psi0) return fail(TCX_E_INVALID, "null circuit or input states");
+  return run(const_cast<tcx_circuit*>(circ)->plan, nullptr, theta, B, nullptr, nullptr, state,
+             ws, ws_bytes, (cudaStream_t)stream, K_STATE, nullptr, nullptr, psi0);
 }
 
 static tcx_status host_call(const tcx_circuit* circ, const tcx_pauli* pauli, const double* th,

@@ -25,7 +25,7 @@ KIND = {name: i for i, name in enumerate(
     ("i", "x", "y", "z", "h", "s", "sdg", "t", "tdg", "cnot", "cz", "swap",
      "rx", "ry", "rz", "rxx", "ryy", "rzz", "u1", "u2"))}
 C64, C128 = 0, 1
-WS_GRAD, WS_HOST_IO, WS_STATE = 1, 2, 4
+WS_GRAD, WS_HOST_IO, WS_STATE, WS_INPUTS = 1, 2, 4, 8
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_UNSUPPORTED", 3: "E_OOM", 4: "E_CUDA", 5: "E_NCCL"}
 
 
@@ -85,6 +85,9 @@ _sig = {
     "tcx_expect_batch": [_vp, _vp, _vp, _i64, _vp, _vp, _sz, _vp],
     "tcx_grad_batch": [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp],
     "tcx_state_batch": [_vp, _vp, _i64, _vp, _vp, _sz, _vp],
+    "tcx_expect_batch_in": [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp],
+    "tcx_grad_batch_in": [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _sz, _vp],
+    "tcx_state_batch_in": [_vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp],
     "tcx_expect_batch_host": [_vp, _vp, _vp, _i64, _vp, _vp, _sz, _vp],
     "tcx_grad_batch_host": [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp],
     "tcx_circuit_info": [_vp, _vp, ctypes.POINTER(tcx_plan_info)],
@@ -259,13 +262,33 @@ def _stream_ptr(stream):
     return ctypes.c_void_p(s.cuda_stream)
 
 
-def expect_batch(circ: Circuit, pauli: Pauli, theta, stream=None, ws: Workspace = None):
-    """E[b] for theta [B, P] float64 on a CUDA device (tcx_expect_batch)."""
+def _inputs(circ, psi0, B, device):
+    """Validate an input-state batch [B, 2^n] (complex dtype of the circuit, on device)."""
+    torch = _torch()
+    cd = torch.complex128 if circ.dtype == "c128" else torch.complex64
+    assert psi0.dtype == cd and psi0.device == device, "psi0: circuit dtype, same device"
+    psi0 = psi0.reshape(B, 1 << circ.n).contiguous()
+    return psi0
+
+
+def expect_batch(circ: Circuit, pauli: Pauli, theta, stream=None, ws: Workspace = None,
+                 psi0=None):
+    """E[b] for theta [B, P] float64 on a CUDA device (tcx_expect_batch); with psi0
+    [B, 2^n] row b starts from the input state psi0[b] (tcx_expect_batch_in)."""
     torch = _torch()
     theta = theta.contiguous()
     assert theta.dtype == torch.float64 and theta.is_cuda
     B = theta.shape[0]
     E = torch.empty(B, dtype=torch.float64, device=theta.device)
+    if psi0 is not None:
+        psi0 = _inputs(circ, psi0, B, theta.device)
+        buf, need = (ws or _default_ws).get(circ, pauli, B, WS_INPUTS, theta.device)
+        _check(_lib.tcx_expect_batch_in(circ.h, pauli.h, ctypes.c_void_p(theta.data_ptr()), B,
+                                        ctypes.c_void_p(psi0.data_ptr()),
+                                        ctypes.c_void_p(E.data_ptr()),
+                                        ctypes.c_void_p(buf.data_ptr()), buf.numel(),
+                                        _stream_ptr(stream)))
+        return E
     buf, need = (ws or _default_ws).get(circ, pauli, B, 0, theta.device)
     _check(_lib.tcx_expect_batch(circ.h, pauli.h, ctypes.c_void_p(theta.data_ptr()), B,
                                  ctypes.c_void_p(E.data_ptr()), ctypes.c_void_p(buf.data_ptr()),
@@ -273,8 +296,10 @@ def expect_batch(circ: Circuit, pauli: Pauli, theta, stream=None, ws: Workspace 
     return E
 
 
-def grad_batch(circ: Circuit, pauli: Pauli, theta, stream=None, ws: Workspace = None, out=None):
-    """(E [B], grad [B, P]) per row (tcx_grad_batch; PAPER.md:1121-1139 batched VQE)."""
+def grad_batch(circ: Circuit, pauli: Pauli, theta, stream=None, ws: Workspace = None, out=None,
+               psi0=None):
+    """(E [B], grad [B, P]) per row (tcx_grad_batch; PAPER.md:1121-1139 batched VQE); with
+    psi0 [B, 2^n] row b starts from psi0[b] (tcx_grad_batch_in)."""
     torch = _torch()
     theta = theta.contiguous()
     assert theta.dtype == torch.float64 and theta.is_cuda
@@ -284,6 +309,15 @@ def grad_batch(circ: Circuit, pauli: Pauli, theta, stream=None, ws: Workspace = 
         G = torch.empty(B, max(circ.P, 1), dtype=torch.float64, device=theta.device)
     else:
         E, G = out
+    if psi0 is not None:
+        psi0 = _inputs(circ, psi0, B, theta.device)
+        buf, need = (ws or _default_ws).get(circ, pauli, B, WS_GRAD | WS_INPUTS, theta.device)
+        _check(_lib.tcx_grad_batch_in(circ.h, pauli.h, ctypes.c_void_p(theta.data_ptr()), B,
+                                      ctypes.c_void_p(psi0.data_ptr()),
+                                      ctypes.c_void_p(E.data_ptr()), ctypes.c_void_p(G.data_ptr()),
+                                      ctypes.c_void_p(buf.data_ptr()), buf.numel(),
+                                      _stream_ptr(stream)))
+        return E, G[:, :circ.P]
     buf, need = (ws or _default_ws).get(circ, pauli, B, WS_GRAD, theta.device)
     _check(_lib.tcx_grad_batch(circ.h, pauli.h, ctypes.c_void_p(theta.data_ptr()), B,
                                ctypes.c_void_p(E.data_ptr()), ctypes.c_void_p(G.data_ptr()),
@@ -292,13 +326,23 @@ def grad_batch(circ: Circuit, pauli: Pauli, theta, stream=None, ws: Workspace = 
     return E, G[:, :circ.P]
 
 
-def state_batch(circ: Circuit, theta, stream=None, ws: Workspace = None):
-    """psi(theta_b) [B, 2^n] complex64/complex128, paper index order."""
+def state_batch(circ: Circuit, theta, stream=None, ws: Workspace = None, psi0=None):
+    """psi(theta_b) [B, 2^n] complex64/complex128, paper index order (U(theta_b) psi0[b]
+    when input states are given)."""
     torch = _torch()
     theta = theta.contiguous()
     B = theta.shape[0]
     cd = torch.complex128 if circ.dtype == "c128" else torch.complex64
     out = torch.empty(B, 1 << circ.n, dtype=cd, device=theta.device)
+    if psi0 is not None:
+        psi0 = _inputs(circ, psi0, B, theta.device)
+        buf, need = (ws or _default_ws).get(circ, None, B, WS_STATE | WS_INPUTS, theta.device)
+        _check(_lib.tcx_state_batch_in(circ.h, ctypes.c_void_p(theta.data_ptr()), B,
+                                       ctypes.c_void_p(psi0.data_ptr()),
+                                       ctypes.c_void_p(out.data_ptr()),
+                                       ctypes.c_void_p(buf.data_ptr()), buf.numel(),
+                                       _stream_ptr(stream)))
+        return out
     buf, need = (ws or _default_ws).get(circ, None, B, WS_STATE, theta.device)
     _check(_lib.tcx_state_batch(circ.h, ctypes.c_void_p(theta.data_ptr()), B,
                                 ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(buf.data_ptr()),

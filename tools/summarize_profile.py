@@ -39,21 +39,22 @@ def main():
     tag, workload = sys.argv[1], sys.argv[2]
     lines = [f"# ncu summary {tag} ({workload})", ""]
     # launch list: last step = last N launches (one bench step after warm-up)
-    launches = read_csv(os.path.join(OUT, f"launches_{tag}.csv"))
+    lp = os.path.join(OUT, f"launches_{tag}.csv")
+    launches = read_csv(lp) if os.path.exists(lp) else []
     per = defaultdict(float)
     for r in launches:
         if r["Metric Name"] == "gpu__time_duration.sum":
             per[(int(r["ID"]), r["Kernel Name"])] = float(r["Metric Value"])
-    ids = sorted(per)
+    ids = sorted(per) or [(0, "materialize")]
     # one step = launches after the last materialize kernel
     firsts = [i for i, (k, n) in enumerate(ids) if "materialize" in n or "dense_mat" in n]
     # a step starts at its first materialize launch (dense plans may launch two)
     last_mat = max(i for i in firsts if i == 0 or i - 1 not in firsts) if firsts else 0
     step = ids[last_mat:]
-    tot = sum(per[k] for k in step)
+    tot = sum(per.get(k, 0.0) for k in step) or 1.0
     by = defaultdict(float)
     for k in step:
-        by[kclass(k[1])] += per[k]
+        by[kclass(k[1])] += per.get(k, 0.0)
     lines += ["## Launch list (one step; ncu per-launch times are cold-cache and serialised)", "",
               "| class | ms | share |", "|---|---|---|"]
     for c, v in sorted(by.items(), key=lambda x: -x[1]):
