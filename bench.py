@@ -309,9 +309,12 @@ def main():
             ach = byt / (kms / 1e3) / 1e9
             roof = {"bound": "hbm", "achieved": ach, "peak": hbm_peak / 1e9, "unit": "GB/s",
                     "frac": ach / (hbm_peak / 1e9)}
-        kname = {"dense": "dense_fwd_kernel (dense k-qubit blocks)",
+        jitk = {"forward": "tcx_jit_fwd_*", "backward": "tcx_jit_bwd_*", "lambda": "tcx_jit_lam_*",
+                "fused": "tcx_jit_mega_*"}
+        kname = {"dense": "dense_fwd_kernel / dense_fwd_tc_kernel (dense k-qubit blocks)",
                  "dense_backward": "dense_bwd_kernel (dense k-qubit blocks, adjoint)"}.get(
-                     dom, f"pass_kernel ({dom} passes)")
+                     dom, (f"{jitk.get(dom, dom)} (per-circuit JIT window passes, {dom})"
+                           if info.get("jit") else f"pass_kernel ({dom} passes)"))
         roof.update({"kernel": kname, "launches": cnt,
                      "share_of_step": kms / total_k,
                      "peak_source": alu_src if roof["bound"] == "alu" else peak_src + " (MEASURED_PEAKS.json hbm_gbs)",
