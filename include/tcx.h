@@ -144,12 +144,14 @@ tcx_status tcx_circuit_build(int32_t n_qubits, int32_t n_params,
 tcx_status tcx_pauli_build(int32_t n_qubits, int32_t n_terms, const uint8_t* codes,
                            const double* weights, tcx_pauli** out);
 
-enum { TCX_WS_GRAD = 1, TCX_WS_HOST_IO = 2, TCX_WS_STATE = 4, TCX_WS_INPUTS = 8 };
+enum { TCX_WS_GRAD = 1, TCX_WS_HOST_IO = 2, TCX_WS_STATE = 4, TCX_WS_INPUTS = 8,
+       TCX_WS_TERMS = 16 };
 
 /* Device workspace bytes for a batch of B rows.  mode: TCX_WS_GRAD for tcx_grad_batch
  * (psi and lambda), 0 for tcx_expect_batch, TCX_WS_STATE for tcx_state_batch; OR
  * TCX_WS_HOST_IO for the *_host entries (adds device room for theta/E/grad), and
- * TCX_WS_INPUTS for the *_in entries (input states). */
+ * TCX_WS_INPUTS for the *_in entries (input states); TCX_WS_TERMS (| TCX_WS_INPUTS) for
+ * tcx_expect_terms_batch. */
 tcx_status tcx_workspace_bytes(const tcx_circuit* circ, const tcx_pauli* pauli, int64_t B,
                                int32_t mode, size_t* bytes);
 
@@ -188,6 +190,16 @@ tcx_status tcx_grad_batch_in(const tcx_circuit* circ, const tcx_pauli* pauli,
 tcx_status tcx_state_batch_in(const tcx_circuit* circ, const double* theta, int64_t B,
                               const void* psi0, void* state, void* ws, size_t ws_bytes,
                               void* cuda_stream);
+
+/* Per-term values (vvag over Pauli structures returns
+ * f(w, v_j) for every term next to the summed gradient, which is tcx_grad_batch with unit
+ * weights): E_terms[b][j] = Re <psi_b|P_j|psi_b> (weights ignored), device [B][n_terms]
+ * float64.  psi0: NULL (|0...0>) or device input states as for the _in entries.  ws sized
+ * with TCX_WS_TERMS (| TCX_WS_INPUTS).  Fixed-order fp64 reductions. */
+tcx_status tcx_expect_terms_batch(const tcx_circuit* circ, const tcx_pauli* pauli,
+                                  const double* theta, int64_t B, const void* psi0,
+                                  double* E_terms, void* ws, size_t ws_bytes,
+                                  void* cuda_stream);
 
 /* End-to-end variants: theta/E/grad are HOST pointers (pinned memory recommended);
  * the call copies theta host->device, runs the same kernels, copies E/grad back and

@@ -105,10 +105,26 @@ struct DenseTcSmem {
   static constexpr int align = 1024;
 };
 
-// K = block qubits (4 or 5): D = 2^K complex rows, KD = 2D real-form inner dimension,
-// N = 2D real-form outputs.
+// 16-byte gathers: complex64 amplitudes are 8 bytes, so every global access moves a pair.
+// Row pairs when index bit 0 is a block bit (amplitudes j, j+1 of a column are adjacent),
+// else column pairs (columns 2p, 2p+1 are adjacent for every row).  Tile = 128 columns.
+__device__ __forceinline__ void sts128(unsigned char* base, uint32_t off, float a, float b, float c,
+                                       float d) {
+  *reinterpret_cast<float4*>(base + off) = make_float4(a, b, c, d);
+}
+// write 4 consecutive K entries (k0 .. k0+3, k0 % 4 == 0) of row m as hi and lo
+__device__ __forceinline__ void put4(unsigned char* sh, unsigned char* sl, int m, int k0, float a,
+                                     float b, float c, float d) {
+  const float ha = tf32_hi(a), hb = tf32_hi(b), hc = tf32_hi(c), hd = tf32_hi(d);
+  const uint32_t off = sw128_off(m, k0, 128);
+  sts128(sh, off, ha, hb, hc, hd);
+  sts128(sl, off, a - ha, b - hb, c - hc, d - hd);
+}
+
+// K = 5 block qubits: D = 32 complex rows, real-form inner dimension and outputs 64.
 template <int K>
 __global__ void __launch_bounds__(128) dense_fwd_tc_kernel(const DenseArgs a) {
+  static_assert(K == 5, "tensor-core dense blocks are k = 5 (16 flop/B, past the FP32 ridge)");
   constexpr int D = 1 << K, KD = 2 * D, N = 2 * D, M = 128;
   constexpr int A_BYTES = M * KD * 4, B_BYTES = N * KD * 4;
   constexpr uint32_t IDESC = umma_idesc_tf32(M, N);
@@ -120,13 +136,13 @@ __global__ void __launch_bounds__(128) dense_fwd_tc_kernel(const DenseArgs a) {
   unsigned char* sBl = sBh + B_BYTES;
   __shared__ uint64_t mbar;
   __shared__ uint32_t s_tmem;
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t b = a.b0 + blockIdx.y;
 
   if (warp == 0) {  // TMEM: N fp32 columns x 128 lanes for the accumulator
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&s_tmem)),
-                 "r"(N < 32 ? 32 : N));
+                 "r"(N));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) mbar_init(&mbar, 1);
@@ -154,39 +170,67 @@ __global__ void __launch_bounds__(128) dense_fwd_tc_kernel(const DenseArgs a) {
   int bits[K];
 #pragma unroll
   for (int i = 0; i < K; ++i) bits[i] = a.bits[i];
+  const bool rowpair = bits[0] == 0;
   const int64_t Nst = 1ll << a.n;
   const int64_t ncols = Nst >> K;
   const int64_t ntiles = (ncols + M - 1) / M;
-  Cx<float>* psi = reinterpret_cast<Cx<float>*>(a.psi) + b * Nst;
+  float* psi = reinterpret_cast<float*>(reinterpret_cast<Cx<float>*>(a.psi) + b * Nst);
   const uint32_t aH = smem_u32(sAh), aL = smem_u32(sAl), bH = smem_u32(sBh), bL = smem_u32(sBl);
 
-  Cx<float> v[D];
+  // per-thread load role: row pairs -> column t, 16 pairs (j, j+1) of rows;
+  // column pairs -> columns (2p, 2p+1), p = t & 63, rows 16h .. 16h+15, h = t >> 6
+  const int cp = tid & 63, hh = tid >> 6;
+  float4 w[16];
   auto load = [&](int64_t tile) {
-    const int64_t c = tile * M + tid;
-    const bool ok = c < ncols;
-    const uint64_t bs = dense_insert<K>(ok ? (uint64_t)c : 0ull, bits);
+    if (rowpair) {
+      const int64_t c = tile * M + tid;
+      const bool ok = c < ncols;
+      const uint64_t bs = dense_insert<K>(ok ? (uint64_t)c : 0ull, bits);
 #pragma unroll
-    for (int j = 0; j < D; ++j) {
-      if (a.init)
-        v[j] = Cx<float>{(ok && c == 0 && j == 0) ? 1.f : 0.f, 0.f};
-      else
-        v[j] = ok ? psi[bs | dense_off<K>(j, bits)] : Cx<float>{0.f, 0.f};
+      for (int q = 0; q < 16; ++q) {
+        if (a.init)
+          w[q] = make_float4((ok && c == 0 && q == 0) ? 1.f : 0.f, 0.f, 0.f, 0.f);
+        else
+          w[q] = ok ? *reinterpret_cast<const float4*>(psi + 2 * (bs | dense_off<K>(2 * q, bits)))
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    } else {
+      const int64_t c = tile * M + 2 * cp;
+      const bool ok = c < ncols;
+      const uint64_t bs = dense_insert<K>(ok ? (uint64_t)c : 0ull, bits);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int j = 16 * hh + q;
+        if (a.init)
+          w[q] = make_float4((ok && c == 0 && j == 0) ? 1.f : 0.f, 0.f, 0.f, 0.f);
+        else
+          w[q] = ok ? *reinterpret_cast<const float4*>(psi + 2 * (bs | dense_off<K>(j, bits)))
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
     }
   };
   uint32_t phase = 0;
   int64_t tile = blockIdx.x;
   if (tile < ntiles) load(tile);
   for (; tile < ntiles; tile += gridDim.x) {
-    // A rows: this thread's column, real parts then imaginary parts, split hi / lo
+    // A rows (hi / lo): K index = j for Re psi_j, D + j for Im psi_j
+    if (rowpair) {
 #pragma unroll
-    for (int j = 0; j < D; j += 2) {
-      // two amplitudes -> 2 re + 2 im floats; write re pair and im pair (8-byte stores)
-      const float r0 = v[j].x, r1 = v[j + 1].x, i0 = v[j].y, i1 = v[j + 1].y;
-      const float hr0 = tf32_hi(r0), hr1 = tf32_hi(r1), hi0 = tf32_hi(i0), hi1 = tf32_hi(i1);
-      *reinterpret_cast<float2*>(sAh + sw128_off(tid, j, M)) = make_float2(hr0, hr1);
-      *reinterpret_cast<float2*>(sAl + sw128_off(tid, j, M)) = make_float2(r0 - hr0, r1 - hr1);
-      *reinterpret_cast<float2*>(sAh + sw128_off(tid, D + j, M)) = make_float2(hi0, hi1);
-      *reinterpret_cast<float2*>(sAl + sw128_off(tid, D + j, M)) = make_float2(i0 - hi0, i1 - hi1);
+      for (int u = 0; u < 8; ++u) {  // rows j = 4u .. 4u+3 live in w[2u] (j, j+1), w[2u+1]
+        const float4 p0 = w[2 * u], p1 = w[2 * u + 1];
+        put4(sAh, sAl, tid, 4 * u, p0.x, p0.z, p1.x, p1.z);
+        put4(sAh, sAl, tid, D + 4 * u, p0.y, p0.w, p1.y, p1.w);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {  // rows j = 16h + 4u .. +3 of columns 2p (x, y) and 2p+1 (z, w)
+        const float4 p0 = w[4 * u], p1 = w[4 * u + 1], p2 = w[4 * u + 2], p3 = w[4 * u + 3];
+        const int k0 = 16 * hh + 4 * u;
+        put4(sAh, sAl, 2 * cp, k0, p0.x, p1.x, p2.x, p3.x);
+        put4(sAh, sAl, 2 * cp, D + k0, p0.y, p1.y, p2.y, p3.y);
+        put4(sAh, sAl, 2 * cp + 1, k0, p0.z, p1.z, p2.z, p3.z);
+        put4(sAh, sAl, 2 * cp + 1, D + k0, p0.w, p1.w, p2.w, p3.w);
+      }
     }
     fence_async_smem();
     tc_fence_before();
@@ -204,31 +248,51 @@ __global__ void __launch_bounds__(128) dense_fwd_tc_kernel(const DenseArgs a) {
       }
       umma_commit(&mbar);
     }
-    // the column this thread wrote, and where its results go
-    const int64_t c = tile * M + tid;
-    const bool ok = c < ncols;
-    const uint64_t bs = dense_insert<K>(ok ? (uint64_t)c : 0ull, bits);
     // next tile's loads overlap the tensor-core work
     if (tile + gridDim.x < ntiles) load(tile + gridDim.x);
     mbar_wait(&mbar, phase);
     phase ^= 1;
     tc_fence_after();
+    // D row m = TMEM lane m = column tile*128 + m: Re out[0..D) then Im out[0..D)
+    float o[N];
     const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-    float o[N];  // real form of U psi_c: Re out[0..D), then Im out[0..D)
 #pragma unroll
     for (int h = 0; h < N / 32; ++h) tmem_ld32(trow + h * 32, o + 32 * h);
     tmem_ld_wait();
-    if (ok) {
+    const int64_t c = tile * M + tid;
+    if (rowpair) {
+      const bool ok = c < ncols;
+      const uint64_t bs = dense_insert<K>(ok ? (uint64_t)c : 0ull, bits);
+      if (ok) {
 #pragma unroll
-      for (int j = 0; j < D; ++j) psi[bs | dense_off<K>(j, bits)] = Cx<float>{o[j], o[D + j]};
+        for (int q = 0; q < 16; ++q)
+          *reinterpret_cast<float4*>(psi + 2 * (bs | dense_off<K>(2 * q, bits))) =
+              make_float4(o[2 * q], o[D + 2 * q], o[2 * q + 1], o[D + 2 * q + 1]);
+      }
+    } else {
+      // lanes 2i / 2i+1 hold adjacent columns; the even lane stores rows 0..15 of both,
+      // the odd lane rows 16..31 (16-byte pairs), exchanging the other half by shuffles
+      const bool odd = lane & 1;
+      const int64_t ce = c & ~1ll;
+      const bool ok = ce < ncols;
+      const uint64_t bs = dense_insert<K>(ok ? (uint64_t)ce : 0ull, bits);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        // compile-time register indices only (a lane-dependent index would spill o[])
+        const float lo_r = o[q], lo_i = o[D + q], hi_r = o[16 + q], hi_i = o[D + 16 + q];
+        const float sr = __shfl_xor_sync(0xffffffffu, odd ? lo_r : hi_r, 1);  // what this lane sends
+        const float si = __shfl_xor_sync(0xffffffffu, odd ? lo_i : hi_i, 1);
+        const int j = odd ? 16 + q : q;   // what this lane stores
+        const float4 v = odd ? make_float4(sr, si, hi_r, hi_i) : make_float4(lo_r, lo_i, sr, si);
+        if (ok) *reinterpret_cast<float4*>(psi + 2 * (bs | dense_off<K>(j, bits))) = v;
+      }
     }
     tc_fence_before();
     __syncthreads();  // TMEM and the A tiles are free for the next tile
   }
   __syncthreads();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(N < 32 ? 32 : N));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(N));
 }
 
 inline constexpr int dense_tc_smem(int K) {

@@ -22,6 +22,7 @@
 #include "kernels.cuh"
 #include "dense.cuh"
 #include "dense_tc.cuh"
+#include "terms.cuh"
 #include "plan.h"
 
 using namespace tcx;
@@ -536,6 +537,15 @@ WsLayout ws_layout(const Plan& P, const Binding* Bd, int64_t B, int kind, bool h
   return w;
 }
 
+// per-term values: CTAs per row (fixed by n alone) and the workspace behind the state layout
+int terms_ctas(const Plan& P) {
+  return (int)std::min<int64_t>(128, std::max<int64_t>(1, (int64_t)1 << std::max(0, P.n - 11)));
+}
+size_t terms_extra(const Plan& P, int64_t B, int T) {
+  return align256((size_t)B * terms_ctas(P) * std::max(T, 1) * 8) +
+         align256(sizeof(TTerm) * std::max(T, 1));
+}
+
 // ---- algorithmic cost model: real flops per amplitude, complex
 // multiply = 6, complex add = 2, real x complex = 2.
 double op_flops(const Op& o, bool bwd) {
@@ -598,7 +608,7 @@ cudaError_t dense_fwd_tc_launch(DenseArgs& a, int64_t rows, cudaStream_t st) {
 template <typename Real>
 cudaError_t dense_fwd(int K, DenseArgs& a, int64_t rows, cudaStream_t st) {
   if (sizeof(Real) == 4 && dense_tc_on(K))
-    return K == 5 ? dense_fwd_tc_launch<5>(a, rows, st) : dense_fwd_tc_launch<4>(a, rows, st);
+    return dense_fwd_tc_launch<5>(a, rows, st);
   switch (K) {
     case 1: dense_fwd_launch<Real, 1>(a, rows, st); break;
     case 2: dense_fwd_launch<Real, 2>(a, rows, st); break;
@@ -640,7 +650,8 @@ struct OneStep {
 
 tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, double* E,
                double* grad, void* state, void* ws, size_t ws_bytes, cudaStream_t st, int kind,
-               const WsLayout* wl_in, const OneStep* one = nullptr, const void* psi0 = nullptr) {
+               const WsLayout* wl_in, const OneStep* one = nullptr, const void* psi0 = nullptr,
+               bool keep_state = false) {
   if (P.gbits > 0 && !one)
     return fail(TCX_E_INVALID, "sharded circuit (global_bits > 0): use tcx_shard_program/exec");
   auto want = [&](int k, int a) { return !one || (one->kind == k && one->arg == a); };
@@ -650,7 +661,7 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
   if (P.P > 0 && !theta) return fail(TCX_E_INVALID, "null theta");
   if (kind != K_STATE && !E) return fail(TCX_E_INVALID, "null E");
   if (kind == K_GRAD && P.P > 0 && !grad) return fail(TCX_E_INVALID, "null grad");
-  if (kind == K_STATE && !state) return fail(TCX_E_INVALID, "null state");
+  if (kind == K_STATE && !state && !keep_state) return fail(TCX_E_INVALID, "null state");
   if (kind == K_GRAD && !P.unitary)
     return fail(TCX_E_UNSUPPORTED, "grad needs unitary payloads (adjoint applies U^dagger)");
   if (kind == K_GRAD && dense_max_k(P) > 4)
@@ -1062,7 +1073,7 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
       finalize_kernel<<<(unsigned)rows, 256, 0, st>>>(f);
       CUDA_TRY(cudaGetLastError());
     }
-  } else if (!one) {
+  } else if (!one && !keep_state) {
     const size_t bytes = (size_t)B * ((size_t)1 << P.n) * 2 * rs;
     if (!P.relabeled) {
       CUDA_TRY(cudaMemcpyAsync(state, W + wl.psi, bytes, cudaMemcpyDeviceToDevice, st));
@@ -1161,6 +1172,12 @@ tcx_status tcx_workspace_bytes(const tcx_circuit* circ, const tcx_pauli* pauli, 
     tcx_status s = binding_for(P, pauli, Bd, nullptr);
     if (s) return s;
   }
+  if (mode & TCX_WS_TERMS) {
+    if (!pauli) return fail(TCX_E_INVALID, "null pauli");
+    *bytes = ws_layout(P, nullptr, B, K_STATE, false, (mode & TCX_WS_INPUTS) != 0).total +
+             terms_extra(P, B, (int)pauli->p.weights.size());
+    return TCX_OK;
+  }
   *bytes = ws_layout(P, Bd.get(), B, kind, (mode & TCX_WS_HOST_IO) != 0,
                      (mode & TCX_WS_INPUTS) != 0).total;
   return TCX_OK;
@@ -1216,6 +1233,59 @@ tcx_status tcx_state_batch_in(const tcx_circuit* circ, const double* theta, int6
   if (!circ || !psi0) return fail(TCX_E_INVALID, "null circuit or input states");
   return run(const_cast<tcx_circuit*>(circ)->plan, nullptr, theta, B, nullptr, nullptr, state,
              ws, ws_bytes, (cudaStream_t)stream, K_STATE, nullptr, nullptr, psi0);
+}
+
+tcx_status tcx_expect_terms_batch(const tcx_circuit* circ, const tcx_pauli* pauli,
+                                  const double* theta, int64_t B, const void* psi0,
+                                  double* E_terms, void* ws, size_t ws_bytes, void* stream) {
+  g_err.clear();
+  if (!circ || !pauli || !E_terms) return fail(TCX_E_INVALID, "null argument");
+  Plan& P = const_cast<tcx_circuit*>(circ)->plan;
+  const Pauli& H = pauli->p;
+  if (H.n != P.n) return fail(TCX_E_INVALID, "pauli n_qubits != circuit n_qubits");
+  if (P.gbits > 0) return fail(TCX_E_UNSUPPORTED, "per-term values of a sharded state");
+  if (B <= 0) return fail(TCX_E_INVALID, "B must be > 0");
+  const int T = (int)H.weights.size();
+  const WsLayout wl = ws_layout(P, nullptr, B, K_STATE, false, psi0 != nullptr);
+  const size_t need = wl.total + terms_extra(P, B, T);
+  if (!ws || ws_bytes < need)
+    return fail(TCX_E_INVALID, "workspace too small: need " + std::to_string(need) + " bytes");
+  cudaStream_t st = (cudaStream_t)stream;
+  tcx_status s = run(P, nullptr, theta, B, nullptr, nullptr, nullptr, ws, ws_bytes, st, K_STATE,
+                     &wl, nullptr, psi0, /*keep_state=*/true);
+  if (s || T == 0) return s;
+  // term masks in the final physical layout (SWAP relabels applied)
+  std::vector<TTerm> tt(T);
+  for (int j = 0; j < T; ++j) {
+    TTerm t{};
+    for (int q = 0; q < P.n; ++q) {
+      const int c = H.codes[(size_t)j * P.n + q];
+      const uint64_t m = 1ull << P.layout[q];
+      if (c == 1 || c == 2) t.x |= m;
+      if (c == 2 || c == 3) t.zy |= m;
+      if (c == 2) t.ny++;
+    }
+    tt[j] = t;
+  }
+  char* W = (char*)ws;
+  double* part = (double*)(W + wl.total);
+  TTerm* dterms = (TTerm*)(W + wl.total + align256((size_t)B * terms_ctas(P) * std::max(T, 1) * 8));
+  CUDA_TRY(cudaMemcpyAsync(dterms, tt.data(), sizeof(TTerm) * T, cudaMemcpyHostToDevice, st));
+  const int S = terms_ctas(P);
+  const int64_t kMaxRows = 65535;
+  for (int64_t b0 = 0; b0 < B; b0 += kMaxRows) {
+    const int64_t rows = std::min(kMaxRows, B - b0);
+    if (P.dtype == TCX_C128)
+      terms_kernel<double><<<dim3(S, (unsigned)rows), 256, 0, st>>>(
+          (const Cx<double>*)(W + wl.psi), P.n, dterms, T, part, b0);
+    else
+      terms_kernel<float><<<dim3(S, (unsigned)rows), 256, 0, st>>>(
+          (const Cx<float>*)(W + wl.psi), P.n, dterms, T, part, b0);
+    CUDA_TRY(cudaGetLastError());
+    terms_sum_kernel<<<dim3((T + 127) / 128, (unsigned)rows), 128, 0, st>>>(part, E_terms, S, T, b0);
+    CUDA_TRY(cudaGetLastError());
+  }
+  return TCX_OK;
 }
 
 static tcx_status host_call(const tcx_circuit* circ, const tcx_pauli* pauli, const double* th,

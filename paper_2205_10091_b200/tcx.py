@@ -25,7 +25,7 @@ KIND = {name: i for i, name in enumerate(
     ("i", "x", "y", "z", "h", "s", "sdg", "t", "tdg", "cnot", "cz", "swap",
      "rx", "ry", "rz", "rxx", "ryy", "rzz", "u1", "u2"))}
 C64, C128 = 0, 1
-WS_GRAD, WS_HOST_IO, WS_STATE, WS_INPUTS = 1, 2, 4, 8
+WS_GRAD, WS_HOST_IO, WS_STATE, WS_INPUTS, WS_TERMS = 1, 2, 4, 8, 16
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_UNSUPPORTED", 3: "E_OOM", 4: "E_CUDA", 5: "E_NCCL"}
 
 
@@ -88,6 +88,7 @@ _sig = {
     "tcx_expect_batch_in": [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp],
     "tcx_grad_batch_in": [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _sz, _vp],
     "tcx_state_batch_in": [_vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp],
+    "tcx_expect_terms_batch": [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp],
     "tcx_expect_batch_host": [_vp, _vp, _vp, _i64, _vp, _vp, _sz, _vp],
     "tcx_grad_batch_host": [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp],
     "tcx_circuit_info": [_vp, _vp, ctypes.POINTER(tcx_plan_info)],
@@ -348,6 +349,30 @@ def state_batch(circ: Circuit, theta, stream=None, ws: Workspace = None, psi0=No
                                 ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(buf.data_ptr()),
                                 buf.numel(), _stream_ptr(stream)))
     return out
+
+
+def expect_terms_batch(circ: Circuit, pauli: Pauli, theta, stream=None, ws: Workspace = None,
+                       psi0=None):
+    """E_terms [B, T]: Re <psi_b|P_j|psi_b> for every term (weights ignored;
+    tcx_expect_terms_batch, PAPER.md:1046-1084)."""
+    torch = _torch()
+    theta = theta.contiguous()
+    assert theta.dtype == torch.float64 and theta.is_cuda
+    B = theta.shape[0]
+    T = int(pauli.weights.size)
+    out = torch.empty(B, max(T, 1), dtype=torch.float64, device=theta.device)
+    mode = WS_TERMS
+    p0 = None
+    if psi0 is not None:
+        p0 = _inputs(circ, psi0, B, theta.device)
+        mode |= WS_INPUTS
+    buf, need = (ws or _default_ws).get(circ, pauli, B, mode, theta.device)
+    _check(_lib.tcx_expect_terms_batch(circ.h, pauli.h, ctypes.c_void_p(theta.data_ptr()), B,
+                                       ctypes.c_void_p(p0.data_ptr()) if p0 is not None else None,
+                                       ctypes.c_void_p(out.data_ptr()),
+                                       ctypes.c_void_p(buf.data_ptr()), buf.numel(),
+                                       _stream_ptr(stream)))
+    return out[:, :T]
 
 
 def grad_batch_host(circ: Circuit, pauli: Pauli, theta_host: np.ndarray, E_host=None,

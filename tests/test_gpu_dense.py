@@ -133,3 +133,27 @@ def test_dense_k5_c64_tensor_core_multi_tile(tc, n, B):
     ref = orc.state(c, np.zeros(0))
     for b in range(B):
         assert np.abs(psi[b] - ref).max() <= state_tol("c64", len(c.gates))
+
+
+@pytest.mark.parametrize("low", [True, False])
+def test_dense_k5_c64_tensor_core_pair_modes(tc, low):
+    """The tcgen05 kernel moves 16-byte pairs: row pairs when index bit 0 (qubit n-1) is a
+    block bit, column pairs otherwise; one 5-qubit block on the lowest / highest qubits."""
+    n = 12
+    qs = list(range(n - 5, n)) if low else list(range(5))
+    rng = np.random.default_rng(17 + low)
+    c = W.Circuit(n, 0)
+    for q in range(n):
+        c.add("h", q)
+    for _ in range(40):
+        a, b = rng.choice(qs, 2, replace=False)
+        kind = ["rx", "ry", "rz", "cnot", "cz", "rxx"][rng.integers(6)]
+        if kind in ("cnot", "cz", "rxx"):
+            c.add(kind, int(a), int(b), coeff=float(rng.uniform(-3, 3)))
+        else:
+            c.add(kind, int(a), coeff=float(rng.uniform(-3, 3)))
+    C = tc.Circuit(c, "c64", dense_k=5)
+    psi = tc.state_batch(C, _th(np.zeros((2, 0)))).cpu().numpy()
+    ref = orc.state(c, np.zeros(0))
+    for b in range(2):
+        assert np.abs(psi[b] - ref).max() <= state_tol("c64", len(c.gates))
