@@ -1148,6 +1148,19 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
           ko.nterm = (int16_t)o.terms.size();
           ko.term = (int)P.kterms.size() - pass.kterm_begin;
           ko.a = o.lut ? 1 : 0;  // JIT: table-driven phase (one weight class)
+          {
+            std::set<uint32_t> rm;  // register-slot masks (the kernels' phase groups)
+            for (auto& tm : o.terms) {
+              uint32_t m = 0;
+              for (int b = 0; b < P.n; ++b)
+                if (tm.mask >> b & 1) {
+                  const int sl = loc[b] >= 0 ? slot_of(b) : -1;
+                  if (sl >= 0) m |= 1u << sl;
+                }
+              rm.insert(m);
+            }
+            o.ngroups = (int)rm.size();
+          }
           for (size_t i = 0; i < o.terms.size(); ++i) {
             KTerm kt;
             std::memset(&kt, 0, sizeof(kt));

@@ -51,6 +51,8 @@ struct Op {
   int nslots = 0;                 // DIAG: distinct gradient slots
   bool has_param = false;
   bool lut = false;  // DIAG: one weight class (param, |w|); phase from a (T+1)-entry table
+  int ngroups = 0;   // DIAG (not LUT): distinct register-slot masks of its terms = complex
+                     // multiplies per amplitude in the kernels (cost model)
   // layout (filled by the scheduler)
   int pass = -1;
   int mat_off = 0, mat_len = 0;  // Reals in the per-theta table

@@ -560,7 +560,12 @@ double op_flops(const Op& o, bool bwd) {
       return bwd ? 28.0 + (o.has_param ? 12.0 : 0.0) : 14.0;
     case OP_U2F: return bwd ? 60.0 : 30.0;
     case OP_CX: return 0.0;
-    default: return bwd ? 12.0 * nt + 2.0 * npar : 6.0 * nt;
+    default:
+      // one complex multiply per amplitude per phase group (LUT: one table entry); the
+      // backward conjugate-multiplies psi and lambda and accumulates Im(lambda* psi) terms
+      if (o.lut) return bwd ? 12.0 + (o.has_param ? 4.0 : 0.0) : 6.0;
+      (void)nt;
+      return bwd ? 12.0 * std::max(o.ngroups, 1) + 2.0 * npar : 6.0 * std::max(o.ngroups, 1);
   }
 }
 double pass_flops(const Plan& P, const PassInfo& p, bool bwd) {
