@@ -291,6 +291,23 @@ def test_cfg2_full_batch_sampled_rows(tc):
     check_grad(G[rows], Gr, H, c, dt, "cfg2 grad")
 
 
+@pytest.mark.slow
+def test_cfg3_full_batch_sampled_row(tc):
+    """configs[2] at full size in the bench launch configuration (QAOA n=24, p=5, B=256,
+    c64): E and the (gamma, beta) gradient of one sampled row against the oracle; every
+    row satisfies 0 <= <C> <= |E| (the cut value is a count of edges)."""
+    name, c, H, th, dt = W.config(2)
+    E, G, _ = run_grad(tc, c, H, th, dt)
+    assert np.isfinite(E).all() and np.isfinite(G).all()
+    n_edges = float(H.weights[0]) * 2 if (H.codes[0] == 0).all() else None
+    if n_edges:
+        assert (E >= -1e-4).all() and (E <= n_edges + 1e-4).all()
+    rows = [131]
+    Er, Gr = orc.value_grad_batch(c, H, th[rows], nthreads=1)
+    check_E(E[rows], Er, H, dt, "cfg3 E")
+    check_grad(G[rows], Gr, H, c, dt, "cfg3 grad")
+
+
 # --------------------------------------------------------------- semantics
 def test_deterministic_and_batch_invariant(tc):
     c, H = W.hea(13, 3), W.heisenberg(13)
