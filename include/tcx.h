@@ -124,6 +124,7 @@ typedef struct {
     int64_t mat_reals;        /* per-theta materialised matrix entries */
     int32_t dense_k;          /* dense block size cap (0: no dense blocks) */
     int32_t dense_blocks;     /* dense k-qubit block passes (each one read+write of psi) */
+    int32_t init_h;           /* leading H gates folded into the initial |+> state */
 } tcx_plan_info;
 
 typedef struct tcx_circuit tcx_circuit;

@@ -88,6 +88,8 @@ struct PassArgs {
   int group_count, e_units, e_index;
   int mode, tiles_per_cta, last_is_top;
   int64_t b0;
+  uint64_t init_hmask;     // M_INIT: leading H gates folded into the initial state |+> on
+  double init_amp;         //   these bits, amplitude init_amp = 2^(-popc/2) (plan.cpp)
 };
 
 struct SmemLayout {

@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(512, 1) pass_kernel(const PassArgs a) {
     if (mode & M_INIT) {
 #pragma unroll
       for (int j = 0; j < NR; ++j) {
-        v[j].x = (gidx(top, j) | a.gbase) == 0 ? Real(1) : Real(0);
+        v[j].x = ((gidx(top, j) | a.gbase) & ~a.init_hmask) == 0 ? Real(a.init_amp) : Real(0);
         v[j].y = 0;
       }
     } else if (mode & M_LOAD_PSI) {

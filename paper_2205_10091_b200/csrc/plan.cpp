@@ -865,8 +865,23 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
     return at;
   };
   if (P.dense_k > 0) build_dense(P, gates, G, pos, payload_copy);
+  // Leading H gates (the first gate on a still-|0> qubit) fold into the initial state: the
+  // first pass writes |+> on those bits (amplitude 2^(-m/2)) instead of applying them, as
+  // QAOA's H^n layer (PAPER.md:391 default input, SURVEY §8d cfg3 "H layer folded into a
+  // write-only init").  The _in entries (caller input states) apply them explicitly.
+  static const bool hfold = getenv("TCX_NO_HFOLD") == nullptr;
+  std::vector<char> touched(n, 0);
   for (int64_t g = 0; g < G && P.dense_k == 0; ++g) {
     const tcx_gate& x = gates[g];
+    if (hfold && x.kind == TCX_H && !touched[x.q0]) {
+      P.init_hmask |= 1ull << pos[x.q0];
+      touched[x.q0] = 1;
+      continue;
+    }
+    if (x.kind != TCX_SWAP && x.kind != TCX_I) {
+      touched[x.q0] = 1;
+      if (is_2q(x.kind)) touched[x.q1] = 1;
+    }
     if (!is_2q(x.kind)) {
       if (x.kind == TCX_I) continue;
       Constituent cn{x.kind, is_rot(x.kind) ? x.param : -1, x.coeff, -1, -1};
@@ -941,6 +956,7 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
     }
   }
   for (int b = 0; b < n; ++b) L.close(b);
+  P.init_amp = std::pow(2.0, -0.5 * (double)popc64(P.init_hmask));
   for (auto& op : P.ops)
     if (op.type == OP_DIAG) normalize_diag(op);
   for (int q = 0; q < n; ++q) P.layout[q] = pos[q];

@@ -180,6 +180,8 @@ struct Plan {
   int tpc = 1;                   // tiles per CTA (depends on the tile count only, never on B)
   int jit_nsub = 1;              // lock-stepped sub-tiles per CTA in JIT kernels
 
+  uint64_t init_hmask = 0;         // leading H gates folded into the initial state (bits)
+  double init_amp = 1.0;           // 2^(-popc(init_hmask)/2)
   int dense_k = 0;                 // > 0: gates run as dense k-qubit blocks (tcx_build_opts)
   std::vector<DBlock> dblocks;     // in execution order (before the window passes)
   std::vector<DGate> dgates;

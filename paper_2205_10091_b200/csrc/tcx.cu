@@ -239,6 +239,23 @@ __global__ void finalize_kernel(const FinArgs a) {
   }
 }
 
+// H on one index bit of every row (input states of a plan whose leading H gates were
+// folded into the |+> initial state: the _in entries apply them explicitly)
+template <typename Real>
+__global__ void hadamard_bit_kernel(Cx<Real>* psi, int n, int bit, int64_t pairs_total) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= pairs_total) return;
+  const int64_t half = (int64_t)1 << (n - 1);
+  const int64_t b = i / half, p = i % half;
+  const int64_t lo = p & (((int64_t)1 << bit) - 1);
+  const int64_t r0 = ((p >> bit) << (bit + 1)) | lo, r1 = r0 | ((int64_t)1 << bit);
+  Cx<Real>* s = psi + (b << n);
+  const Real k = Real(0.70710678118654752440);
+  const Cx<Real> x0 = s[r0], x1 = s[r1];
+  s[r0] = Cx<Real>{k * (x0.x + x1.x), k * (x0.y + x1.y)};
+  s[r1] = Cx<Real>{k * (x0.x - x1.x), k * (x0.y - x1.y)};
+}
+
 // gather physical -> paper index order (only when SWAP relabels moved qubits)
 template <typename Real>
 __global__ void export_kernel(const Cx<Real>* src, Cx<Real>* dst, int n, int64_t total,
@@ -721,6 +738,16 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
     if (wl.mega) return fail(TCX_E_INVALID, "workspace sized without TCX_WS_INPUTS");
     CUDA_TRY(cudaMemcpyAsync(W + wl.psi, psi0, (size_t)B * ((size_t)1 << P.n) * 2 * rs,
                              cudaMemcpyDeviceToDevice, st));
+    const int64_t pairs = B << (P.n - 1);
+    for (int bit = 0; bit < P.n; ++bit) {  // leading H gates folded into the plan's init
+      if (!(P.init_hmask >> bit & 1)) continue;
+      const unsigned blocks = (unsigned)((pairs + 255) / 256);
+      if (c128)
+        hadamard_bit_kernel<double><<<blocks, 256, 0, st>>>((Cx<double>*)(W + wl.psi), P.n, bit, pairs);
+      else
+        hadamard_bit_kernel<float><<<blocks, 256, 0, st>>>((Cx<float>*)(W + wl.psi), P.n, bit, pairs);
+      CUDA_TRY(cudaGetLastError());
+    }
   }
   // ---- dense block matrices: row-independent blocks once, parameterised ones per row
   const bool dense = !P.dblocks.empty();
@@ -792,6 +819,8 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
     a.mode = mode;
     a.tiles_per_cta = tiles_per_cta(P);
     a.last_is_top = 1;
+    a.init_hmask = P.init_hmask;
+    a.init_amp = P.init_amp;
   };
   auto set_pass = [&](PassArgs& a, const PassInfo& p, bool with_ops) {
     a.stages = (const KStage*)DT->kstages.p + p.stage_begin;
@@ -1379,6 +1408,7 @@ tcx_status tcx_circuit_info(const tcx_circuit* circ, const tcx_pauli* pauli, tcx
   o->mat_reals = P.mat_total;
   o->dense_k = P.dense_k;
   o->dense_blocks = (int)P.dblocks.size();
+  o->init_h = __builtin_popcountll(P.init_hmask);
   if (!P.dblocks.empty()) {  // the trailing E / lambda pass has no gates: no backward launch
     int nb = 0;
     for (auto& p : P.passes) nb += p.ops.empty() ? 0 : 1;

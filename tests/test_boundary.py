@@ -178,3 +178,15 @@ def test_dense_plan_blocks():
         m.Circuit(c2, "c64", dense_k=6)
     with pytest.raises(m.TcxError):
         m.Circuit(W.hea(8, 1), "c64", dense_k=2, global_bits=1)
+
+
+def test_leading_h_folded_into_init():
+    """QAOA's H^n layer is folded into the initial |+> state; an H after
+    another gate on the same qubit is not; dense plans never fold."""
+    from paper_2205_10091_b200 import tcx as m
+    name, c, H, th, dt = W.config(2)
+    info = m.Circuit(c, dt).info()
+    assert info["init_h"] == c.n
+    c2 = W.Circuit(3, 1).add("h", 0).add("rx", 1, param=0, coeff=1.0).add("h", 1).add("h", 2)
+    assert m.Circuit(c2, "c64").info()["init_h"] == 2          # qubits 0 and 2
+    assert m.Circuit(c2, "c64", dense_k=2).info()["init_h"] == 0
