@@ -878,7 +878,9 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
       touched[x.q0] = 1;
       continue;
     }
-    if (x.kind != TCX_SWAP && x.kind != TCX_I) {
+    if (x.kind == TCX_SWAP) {  // the qubits exchange states (a relabel below)
+      std::swap(touched[x.q0], touched[x.q1]);
+    } else if (x.kind != TCX_I) {
       touched[x.q0] = 1;
       if (is_2q(x.kind)) touched[x.q1] = 1;
     }

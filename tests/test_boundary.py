@@ -190,3 +190,11 @@ def test_leading_h_folded_into_init():
     c2 = W.Circuit(3, 1).add("h", 0).add("rx", 1, param=0, coeff=1.0).add("h", 1).add("h", 2)
     assert m.Circuit(c2, "c64").info()["init_h"] == 2          # qubits 0 and 2
     assert m.Circuit(c2, "c64", dense_k=2).info()["init_h"] == 0
+
+
+def test_h_fold_follows_swap_relabels():
+    """SWAP exchanges the qubits' states, so after SWAP(a, b) with only `a` touched, an H
+    on b is not a leading H (b now carries a's state) while an H on a is."""
+    from paper_2205_10091_b200 import tcx as m
+    c = W.Circuit(3, 1).add("rx", 0, param=0, coeff=1.0).add("swap", 0, 1).add("h", 1).add("h", 0)
+    assert m.Circuit(c, "c64").info()["init_h"] == 1
