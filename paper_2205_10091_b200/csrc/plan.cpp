@@ -984,6 +984,9 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
       shard_swap_perm(n, gb, perm);
       for (size_t i = 0; i < P.ops.size(); ++i)
         if (!S.done[i]) remap_op(P.ops[i], perm, n);
+      // no pass has run yet: the first pass (which writes the initial state) runs in the
+      // new layout, so the folded-H bits move with the qubits
+      if (P.passes.empty()) P.init_hmask = remap_mask(P.init_hmask, perm, n);
       for (int q = 0; q < n; ++q) pos[q] = perm[pos[q]];
       ++seg;
       swapped_last = true;
