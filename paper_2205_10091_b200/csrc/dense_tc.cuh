@@ -20,7 +20,7 @@
 // its column's 2^k amplitudes (coalesced across the warp over the non-block bits), splits
 // them and writes the hi / lo rows of A into shared memory in the canonical K-major
 // SWIZZLE_128B layout (8-row x 128-byte atoms, 16-byte chunk c of row r stored at c ^ (r & 7));
-// one elected thread issues 3 * (K / 8) tcgen05.mma and commits to an mbarrier; while the
+// one elected thread issues 3 * (2^(k+1) / 8) = 24 tcgen05.mma and commits to an mbarrier; while the
 // tensor core runs, every thread already loads its column of the next tile; then each warp
 // reads its 32 TMEM lanes back (tcgen05.ld 32x32b) and scatters the outputs in place.
 #pragma once
@@ -100,10 +100,6 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int k, int rows) {
   const int chunk = (kk >> 2) ^ (r & 7);
   return (uint32_t)(atom * rows * 128 + r * 128 + chunk * 16 + (kk & 3) * 4);
 }
-
-struct DenseTcSmem {
-  static constexpr int align = 1024;
-};
 
 // 16-byte gathers: complex64 amplitudes are 8 bytes, so every global access moves a pair.
 // Row pairs when index bit 0 is a block bit (amplitudes j, j+1 of a column are adjacent),
