@@ -615,6 +615,25 @@ bool dense_tc_on(int K) {
   }();
   return mode != 0 && K == 5;
 }
+int dense_tc_variant() {  // 1: one role per thread, 2 CTAs per SM; 2: warp-specialised
+  static const int v = [] {
+    const char* e = getenv("TCX_DENSE_TC_WS");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+template <int K>
+cudaError_t dense_fwd_tc_ws_launch(DenseArgs& a, int64_t rows, cudaStream_t st) {
+  const int sm = dense_tc_ws_smem(K);
+  cudaError_t e = cudaFuncSetAttribute(dense_fwd_tc_ws_kernel<K>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  if (e != cudaSuccess) return e;
+  const int64_t ncols = ((int64_t)1 << a.n) >> K;
+  const int64_t tiles = (ncols + 127) / 128;
+  const int64_t gx = std::max<int64_t>(1, std::min<int64_t>(tiles, std::max<int64_t>(1, 148 / rows)));
+  dense_fwd_tc_ws_kernel<K><<<dim3((unsigned)gx, (unsigned)rows), 256, sm, st>>>(a);
+  return cudaGetLastError();
+}
 template <int K>
 cudaError_t dense_fwd_tc_launch(DenseArgs& a, int64_t rows, cudaStream_t st) {
   const int sm = dense_tc_smem(K);
@@ -630,7 +649,8 @@ cudaError_t dense_fwd_tc_launch(DenseArgs& a, int64_t rows, cudaStream_t st) {
 template <typename Real>
 cudaError_t dense_fwd(int K, DenseArgs& a, int64_t rows, cudaStream_t st) {
   if (sizeof(Real) == 4 && dense_tc_on(K))
-    return dense_fwd_tc_launch<5>(a, rows, st);
+    return dense_tc_variant() == 2 ? dense_fwd_tc_ws_launch<5>(a, rows, st)
+                                   : dense_fwd_tc_launch<5>(a, rows, st);
   switch (K) {
     case 1: dense_fwd_launch<Real, 1>(a, rows, st); break;
     case 2: dense_fwd_launch<Real, 2>(a, rows, st); break;
