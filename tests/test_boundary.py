@@ -145,6 +145,20 @@ def test_no_cpu_fallback(tcx):
                                  ctypes.cast(buf, ctypes.c_void_p), len(buf), None)
     assert rc == 4, tcx.last_error()
     assert "no CUDA device" in tcx.last_error()
+    # the input-state and per-term entries as well (dense and window plans)
+    p0 = np.zeros(2 << c.n, dtype=np.float32)
+    Et = np.zeros(P_terms := len(W.tfim_zz_x(4).weights))
+    for Cx in (C, tcx.Circuit(c, "c64", dense_k=2)):
+        rc = tcx._lib.tcx_grad_batch_in(Cx.h, P.h, ctypes.c_void_p(th.ctypes.data), 1,
+                                        ctypes.c_void_p(p0.ctypes.data),
+                                        ctypes.c_void_p(E.ctypes.data), ctypes.c_void_p(g.ctypes.data),
+                                        ctypes.cast(buf, ctypes.c_void_p), len(buf), None)
+        assert rc == 4, tcx.last_error()
+        rc = tcx._lib.tcx_expect_terms_batch(Cx.h, P.h, ctypes.c_void_p(th.ctypes.data), 1, None,
+                                             ctypes.c_void_p(Et.ctypes.data),
+                                             ctypes.cast(buf, ctypes.c_void_p), len(buf), None)
+        assert rc == 4, tcx.last_error()
+    assert P_terms == 7
 
 
 def test_bench_reference_arm_runs():
