@@ -140,8 +140,12 @@ struct Binding {        // (circuit, pauli) specific lambda schedule
   std::vector<LamUnit> units;
   bool xmask_ok = true;
   std::string err;
-  // device copies (per device)
+  // device copies (per device), released by the destructor (tcx.cu)
   std::map<int, std::pair<void*, void*>> dev;  // device -> (groups, pterms)
+  Binding() = default;
+  Binding(const Binding&) = delete;
+  Binding& operator=(const Binding&) = delete;
+  ~Binding();
 };
 
 struct DeviceTables;

@@ -286,6 +286,8 @@ struct DeviceTables {
   DevBuf dblocks, dgates, dpblocks;  // dense k-qubit blocks (dense.cuh)
   std::map<std::string, CUfunction> jit;   // key (jit.h)
   std::map<std::string, size_t> jit_smem;  // dynamic smem opted in per function
+  std::vector<CUmodule> modules;           // loaded JIT modules (unloaded with the plan)
+  ~DeviceTables();
 };
 }  // namespace tcx
 
@@ -310,6 +312,7 @@ tcx_status upload(DevBuf& d, const std::vector<T>& v) {
 struct Drv {
   bool ok = false;
   CUresult (*moduleLoadData)(CUmodule*, const void*);
+  CUresult (*moduleUnload)(CUmodule);
   CUresult (*moduleGetFunction)(CUfunction*, CUmodule, const char*);
   CUresult (*launchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
                            unsigned, CUstream, void**, void**);
@@ -329,6 +332,7 @@ Drv& drv() {
              q == cudaDriverEntryPointSuccess;
     };
     D.ok = get("cuModuleLoadData", (void**)&D.moduleLoadData) &&
+           get("cuModuleUnload", (void**)&D.moduleUnload) &&
            get("cuModuleGetFunction", (void**)&D.moduleGetFunction) &&
            get("cuLaunchKernel", (void**)&D.launchKernel) &&
            get("cuFuncSetAttribute", (void**)&D.funcSetAttribute) &&
@@ -336,6 +340,26 @@ Drv& drv() {
   });
   return D;
 }
+
+}  // namespace
+
+tcx::DeviceTables::~DeviceTables() {
+  Drv& D = drv();
+  if (D.ok)
+    for (CUmodule m : modules) D.moduleUnload(m);
+}
+tcx::Binding::~Binding() {
+  for (auto& kv : dev) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(kv.first);
+    cudaFree(kv.second.first);
+    cudaFree(kv.second.second);
+    cudaSetDevice(cur);
+  }
+}
+
+namespace {
 
 // Tensor map of a [B][2^n] state buffer viewed through a pass window (plan.cpp tma_dims):
 // 8-byte elements, box = one tile, no swizzle (the kernels read the dense tile in the
@@ -420,6 +444,7 @@ tcx_status jit_function(Plan& P, DeviceTables* DT, const std::string& key, CUfun
   if (D.moduleGetFunction(&fn, m, k.name.c_str()) != CUDA_SUCCESS)
     return fail(TCX_E_CUDA, "cuModuleGetFunction failed for " + k.name);
   std::lock_guard<std::mutex> lk(P.mu);
+  DT->modules.push_back(m);
   DT->jit[key] = fn;
   DT->jit_smem[key] = 0;
   *f = fn;
