@@ -69,6 +69,12 @@ typedef enum {
     TCX_RX, TCX_RY, TCX_RZ, TCX_RXX, TCX_RYY, TCX_RZZ,
     /* fixed payload matrices (PAPER.md:355-360 c.unitary): 2x2 / 4x4 */
     TCX_U1, TCX_U2,
+    /* Monte Carlo trajectory of a depolarizing channel (PAPER.md:652-700 unitary_kraus with an
+     * external `status`): 1 qubit, param = the theta column holding the row's
+     * status x in [0, 1), payload = 2 complex elements (px + i py, pz + 0i).  [0, 1) is split
+     * in the paper's Kraus order I, X, Y, Z: x < 1-px-py-pz -> I, < 1-py-pz -> X, < 1-pz -> Y,
+     * else Z.  Not differentiable: its status column gets no gradient contribution. */
+    TCX_DEPOL,
     TCX_NKINDS
 } tcx_gate_kind;
 

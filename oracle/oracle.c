@@ -41,7 +41,7 @@ enum {
     OK_I = 0, OK_X, OK_Y, OK_Z, OK_H, OK_S, OK_SDG, OK_T, OK_TDG,
     OK_CNOT, OK_CZ, OK_SWAP,
     OK_RX, OK_RY, OK_RZ, OK_RXX, OK_RYY, OK_RZZ,
-    OK_U1, OK_U2, OK_NKINDS
+    OK_U1, OK_U2, OK_DEPOL, OK_NKINDS
 };
 
 /* ---------------------------------------------------------------- matrices */
@@ -126,6 +126,19 @@ static void gate_matrix(int kind, double a, const double *payload, cplx *m)
         for (int i = 0; i < d * d; ++i)
             m[i] = payload[2 * i] + I * payload[2 * i + 1];
         break;
+    case OK_DEPOL: {
+        /* Monte Carlo trajectory of the depolarizing channel: [0,1) is
+         * partitioned into intervals of lengths 1-px-py-pz, px, py, pz in the order of the
+         * Kraus operators K0 = I, K1 = X, K2 = Y, K3 = Z; the status x = a picks the one
+         * applied.  payload = (px, py, pz, 0). */
+        const double px = payload[0], py = payload[1], pz = payload[2];
+        int w = 0;
+        if (a >= 1.0 - px - py - pz) w = 1;
+        if (a >= 1.0 - py - pz) w = 2;
+        if (a >= 1.0 - pz) w = 3;
+        pauli2(w, m);
+        break;
+    }
     }
 }
 
@@ -194,6 +207,8 @@ int orc_validate(int n, int G, const int *kind, const int *q0, const int *q1,
         if (q0[g] < 0 || q0[g] >= n) return 1 + g;
         if (arity(k) == 2 && (q1[g] < 0 || q1[g] >= n || q1[g] == q0[g])) return 1 + g;
         if (is_rotation(k) && (param[g] < -1 || param[g] >= P)) return 1 + g;
+        if (k == OK_DEPOL && (param[g] < 0 || param[g] >= P || moff[g] < 0 || moff[g] + 2 > nmat))
+            return 1 + g;
         if (k == OK_U1 || k == OK_U2) {
             int64_t need = (k == OK_U1 ? 4 : 16);
             if (moff[g] < 0 || moff[g] + need > nmat) return 1 + g;
@@ -208,6 +223,14 @@ static double angle_of(int g, const int *param, const double *coeff, const doubl
     double a = param[g] >= 0 ? coeff[g] * theta[param[g]] : coeff[g];
     if (g == shift_gate) a += shift;
     return a;
+}
+
+/* the argument gate_matrix takes: the angle, or for OK_DEPOL the row's status theta[param] */
+static double gate_arg(int g, const int *kind, const int *param, const double *coeff,
+                       const double *theta, int shift_gate, double shift)
+{
+    if (kind[g] == OK_DEPOL) return theta[param[g]];
+    return angle_of(g, param, coeff, theta, shift_gate, shift);
 }
 
 /* ------------------------------------------------------------- state() */
@@ -229,7 +252,7 @@ static void state_c(int n, int G, const int *kind, const int *q0, const int *q1,
     }
     for (int g = 0; g < G; ++g) {
         cplx m[16];
-        double a = angle_of(g, param, coeff, theta, shift_gate, shift);
+        double a = gate_arg(g, kind, param, coeff, theta, shift_gate, shift);
         gate_matrix(kind[g], a, moff[g] >= 0 ? mats + 2 * moff[g] : NULL, m);
         apply_matrix(n, psi, kind[g], q0[g], q1[g], m);
     }
@@ -341,7 +364,7 @@ static int value_grad_c(int n, int G, const int *kind, const int *q0, const int 
             grad[param[g]] += coeff[g] * cimag(inner(N, lam, tmp));
         }
         cplx m[16], md[16];
-        double a = angle_of(g, param, coeff, theta, -1, 0.0);
+        double a = gate_arg(g, kind, param, coeff, theta, -1, 0.0);
         gate_matrix(kind[g], a, moff[g] >= 0 ? mats + 2 * moff[g] : NULL, m);
         dagger(m, arity(kind[g]) == 1 ? 2 : 4, md);
         apply_matrix(n, psi, kind[g], q0[g], q1[g], md);

@@ -104,6 +104,15 @@ __device__ void dense_gate_matrix(const DGate& g, const double* th, const double
     case TCX_U2:
       for (int i = 0; i < 16; ++i) m[i] = {fixed[2 * (g.payload + i)], fixed[2 * (g.payload + i) + 1]};
       break;
+    case TCX_DEPOL: {  // Monte Carlo depolarizing: status interval -> I, X, Y, Z
+      const double x = th[g.param], px = fixed[2 * g.payload], py = fixed[2 * g.payload + 1],
+                   pz = fixed[2 * g.payload + 2];
+      if (x < 1.0 - px - py - pz) break;
+      if (x < 1.0 - py - pz) { m[0] = {0, 0}; m[1] = {1, 0}; m[2] = {1, 0}; m[3] = {0, 0}; break; }
+      if (x < 1.0 - pz) { m[0] = {0, 0}; m[1] = {0, -1}; m[2] = {0, 1}; m[3] = {0, 0}; break; }
+      m[3] = {-1, 0};
+      break;
+    }
     default: break;
   }
 }
@@ -452,7 +461,7 @@ __global__ void dense_grad_kernel(const DenseGradArgs a) {
   __syncthreads();
   for (int gi = blk.gate_count - 1; gi >= 0; --gi) {
     const DGate g = a.gates[blk.gate_begin + gi];
-    if (g.param >= 0) {
+    if (g.contrib >= 0) {
       // P_g on local bits (X / Y / Z masks of the rotation generator)
       int xm = 0, ym = 0, zm = 0;
       const int sa = 1 << g.a, sb = g.b >= 0 ? 1 << g.b : 0;

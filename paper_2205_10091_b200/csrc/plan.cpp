@@ -139,7 +139,7 @@ struct Lowerer {
       op.bits = op.need = 1ull << bit;
       op.b0 = bit;
       op.cons = R.cons;
-      for (auto& c : op.cons) op.has_param |= c.param >= 0;
+      for (auto& c : op.cons) op.has_param |= c.param >= 0 && is_rot(c.kind);
       emit(std::move(op));
     }
     R = Run();
@@ -648,7 +648,8 @@ void shard_swap_perm(int n, int g, int* perm) {
 // and blocks on disjoint bits commute, so the emitted sequence equals the gate list.
 // SWAP stays a relabel of the qubit -> bit map (as in the window lowering).
 void build_dense(Plan& P, const tcx_gate* gates, int64_t G, int* pos,
-                 const std::function<int64_t(int64_t, int)>& payload_copy) {
+                 const std::function<int64_t(int64_t, int)>& payload_copy,
+                 const std::function<int64_t(int64_t, int)>& payload_copy_raw) {
   struct Open {
     std::vector<int64_t> g;
     uint64_t mask = 0;
@@ -659,6 +660,7 @@ void build_dense(Plan& P, const tcx_gate* gates, int64_t G, int* pos,
   auto pos_at = [&](int64_t gi) { return gp[(size_t)gi].data(); };
   auto emit = [&](const Open& o) {
     DBlock d{};
+    bool theta_dep = false;
     d.k = popc64(o.mask);
     int loc[64];
     int i = 0;
@@ -675,16 +677,18 @@ void build_dense(Plan& P, const tcx_gate* gates, int64_t G, int* pos,
       dg.kind = x.kind;
       dg.a = loc[pos_at(gi)[0]];
       dg.b = is_2q(x.kind) ? loc[pos_at(gi)[1]] : -1;
-      dg.param = is_rot(x.kind) ? x.param : -1;
+      dg.param = (is_rot(x.kind) || x.kind == TCX_DEPOL) ? x.param : -1;
       dg.coeff = x.coeff;
       dg.payload = -1;
       if (x.kind == TCX_U1) dg.payload = payload_copy(x.payload, 2);
       if (x.kind == TCX_U2) dg.payload = payload_copy(x.payload, 4);
+      if (x.kind == TCX_DEPOL) dg.payload = payload_copy_raw(x.payload, 2);
       dg.contrib = -1;
-      d.has_param |= dg.param >= 0;
+      d.has_param |= dg.param >= 0 && is_rot(x.kind);  // gradient slots
+      theta_dep |= dg.param >= 0;                       // U depends on the theta row
       P.dgates.push_back(dg);
     }
-    d.shared = d.has_param ? 0 : 1;
+    d.shared = theta_dep ? 0 : 1;
     const int m = 1 << (2 * d.k);
     if (d.shared) {
       d.mat_off = P.dmat_shared;
@@ -790,6 +794,14 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
     if (is_rot(x.kind)) {
       if (x.param < -1 || x.param >= Pn) return bad("param out of range");
       if (!std::isfinite(x.coeff)) return bad("non-finite coeff");
+    } else if (x.kind == TCX_DEPOL) {
+      if (x.param < 0 || x.param >= Pn) return bad("depolarizing status column out of range");
+      if (x.payload < 0 || x.payload + 2 > nmat) return bad("payload out of range");
+      const double px = mats[2 * x.payload], py = mats[2 * x.payload + 1],
+                   pz = mats[2 * x.payload + 2];
+      if (!(px >= 0 && py >= 0 && pz >= 0 && px + py + pz <= 1.0 + 1e-12))
+        return bad("depolarizing probabilities must be >= 0 with px + py + pz <= 1");
+      continue;
     } else if (x.param != -1) {
       return bad("param must be -1 for a non-rotation gate");
     }
@@ -858,13 +870,18 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
   int pos[kMaxQubits];
   for (int q = 0; q < n; ++q) pos[q] = n - 1 - q;  // PAPER.md:249 qubit 0 = MSB
   Lowerer L(P);
+  auto payload_copy_raw = [&](int64_t off, int elems) {  // complex elements, no checks
+    int64_t at = (int64_t)P.fixed.size() / 2;
+    for (int64_t e = 0; e < 2 * elems; ++e) P.fixed.push_back(mats[2 * off + e]);
+    return at;
+  };
   auto payload_copy = [&](int64_t off, int d) {
     int64_t at = (int64_t)P.fixed.size() / 2;
     for (int64_t e = 0; e < 2 * d * d; ++e) P.fixed.push_back(mats[2 * off + e]);
     if (!unitary_check(mats + 2 * off, d)) P.unitary = false;
     return at;
   };
-  if (P.dense_k > 0) build_dense(P, gates, G, pos, payload_copy);
+  if (P.dense_k > 0) build_dense(P, gates, G, pos, payload_copy, payload_copy_raw);
   // Leading H gates (the first gate on a still-|0> qubit) fold into the initial state: the
   // first pass writes |+> on those bits (amplitude 2^(-m/2)) instead of applying them, as
   // QAOA's H^n layer (PAPER.md:391 default input, SURVEY §8d cfg3 "H layer folded into a
@@ -886,8 +903,9 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
     }
     if (!is_2q(x.kind)) {
       if (x.kind == TCX_I) continue;
-      Constituent cn{x.kind, is_rot(x.kind) ? x.param : -1, x.coeff, -1, -1};
+      Constituent cn{x.kind, (is_rot(x.kind) || x.kind == TCX_DEPOL) ? x.param : -1, x.coeff, -1, -1};
       if (x.kind == TCX_U1) cn.payload = payload_copy(x.payload, 2);
+      if (x.kind == TCX_DEPOL) cn.payload = payload_copy_raw(x.payload, 2);
       L.add1(pos[x.q0], cn, is_diag1(x.kind));
       continue;
     }
@@ -1243,7 +1261,7 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
         d.coeff = cn.coeff;
         d.payload = cn.payload;
         d.contrib = -1;
-        if (cn.param >= 0) {
+        if (cn.param >= 0 && is_rot(cn.kind)) {
           d.contrib = contrib++;
           contrib_param.push_back(cn.param);
         }
@@ -1307,7 +1325,7 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
     }
   }
   for (auto& dg : P.dgates)
-    if (dg.param >= 0) {
+    if (dg.param >= 0 && is_rot(dg.kind)) {
       dg.contrib = contrib++;
       contrib_param.push_back(dg.param);
     }

@@ -85,6 +85,15 @@ __device__ void gate1(const DCons& c, const double* theta, const double* fixed, 
     case TCX_U1:
       for (int i = 0; i < 4; ++i) g[i] = {fixed[2 * (c.payload + i)], fixed[2 * (c.payload + i) + 1]};
       break;
+    case TCX_DEPOL: {  // status x = theta[param]: I, X, Y, Z on [0,1) in the paper's order
+      const double x = theta[c.param], px = fixed[2 * c.payload], py = fixed[2 * c.payload + 1],
+                   pz = fixed[2 * c.payload + 2];
+      if (x < 1.0 - px - py - pz) break;
+      if (x < 1.0 - py - pz) { g[0] = {0, 0}; g[1] = {1, 0}; g[2] = {1, 0}; g[3] = {0, 0}; break; }
+      if (x < 1.0 - pz) { g[0] = {0, 0}; g[1] = {0, -1}; g[2] = {0, 1}; g[3] = {0, 0}; break; }
+      g[3] = {-1, 0};
+      break;
+    }
     default: break;
   }
 }
@@ -214,7 +223,7 @@ __global__ void finalize_kernel(const FinArgs a) {
     cdd Sfx[4] = {{1, 0}, {0, 0}, {0, 0}, {1, 0}};
     for (int c = g.cons_count - 1; c >= 0; --c) {
       const DCons cn = a.cons[g.cons_begin + c];
-      if (cn.param >= 0) {
+      if (cn.contrib >= 0) {  // differentiable rotations only (not depolarizing statuses)
         cdd Pm[4] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
         if (cn.kind == TCX_RX) { Pm[1] = {1, 0}; Pm[2] = {1, 0}; }
         if (cn.kind == TCX_RY) { Pm[1] = {0, -1}; Pm[2] = {0, 1}; }

@@ -386,3 +386,52 @@ def test_input_state_composition():
     Er, Gr = orc.value_grad_batch(both, H, th)
     np.testing.assert_allclose(E, Er, atol=1e-12)
     np.testing.assert_allclose(G, Gr, atol=1e-12)
+
+
+# ------------------------------ Monte Carlo trajectories
+def test_depolarizing_status_intervals():
+    """unitary_kraus with an external status: [0,1) splits into lengths
+    1-px-py-pz, px, py, pz in the Kraus order I, X, Y, Z; |0> goes to I|0>, X|0>, Y|0>, Z|0>."""
+    px, py, pz = 0.1, 0.2, 0.3
+    c = W.Circuit(1, 1)
+    W.add_depolarizing(c, 0, 0, px, py, pz)
+    expect = {0.05: [1, 0], 0.39: [1, 0], 0.41: [0, 1], 0.55: [0, 1j], 0.69: [0, 1j],
+              0.71: [1, 0], 0.99: [1, 0]}
+    for x, v in expect.items():
+        np.testing.assert_allclose(orc.state(c, np.array([x])), v, atol=0)
+    # Z|0> = |0>: distinguish Z from I on |+>
+    c2 = W.Circuit(1, 1).add("h", 0)
+    W.add_depolarizing(c2, 0, 0, px, py, pz)
+    r = 1 / np.sqrt(2)
+    np.testing.assert_allclose(orc.state(c2, np.array([0.8])), [r, -r], atol=1e-15)
+    np.testing.assert_allclose(orc.state(c2, np.array([0.3])), [r, r], atol=1e-15)
+
+
+def test_depolarizing_trajectory_average_closed_form():
+    """Averaging trajectories over stratified statuses x_k = (k + 1/2)/K reproduces the
+    channel exactly when K * p is integral: on |0>, E<Z> = 1 - 2(px + py); on |+>,
+    E<X> = 1 - 2(py + pz) (the paper's h(0) + depolarizingchannel(0.1, 0.2, 0.3) example)."""
+    px, py, pz, K = 0.1, 0.2, 0.3, 1000
+    xs = ((np.arange(K) + 0.5) / K)[:, None]
+    c = W.Circuit(1, 1)
+    W.add_depolarizing(c, 0, 0, px, py, pz)
+    Ez = orc.expect_batch(c, W.pauli_sum(1, [({0: "Z"}, 1.0)]), xs)
+    assert abs(Ez.mean() - (1 - 2 * (px + py))) < 1e-12
+    c2 = W.Circuit(1, 1).add("h", 0)
+    W.add_depolarizing(c2, 0, 0, px, py, pz)
+    Ex = orc.expect_batch(c2, W.pauli_sum(1, [({0: "X"}, 1.0)]), xs)
+    assert abs(Ex.mean() - (1 - 2 * (py + pz))) < 1e-12
+
+
+def test_noisy_vqe_gradient_per_trajectory():
+    """PAPER.md:1149-1174 (vvag over statuses): for a fixed trajectory the adjoint gradient
+    of the weights equals the parameter shift; status columns get no gradient."""
+    n, d = 4, 2
+    c, H = W.noisy_vqe(n, d), W.tfim_zz_x(n)
+    w = W.thetas(1, 3 * n * d, 7)[0]
+    st = W.statuses(1, n * d, 8)[0]
+    th = np.concatenate([w, st])
+    E, _, g = orc.value_grad(c, H, th)
+    ps = orc.param_shift(c, H, th)
+    np.testing.assert_allclose(g, ps, atol=1e-10)
+    assert np.all(g[3 * n * d:] == 0.0)

@@ -197,6 +197,32 @@ def random_circuit(n: int, n_gates: int, seed: int, n_params: int = 8,
     return c
 
 
+def add_depolarizing(c: Circuit, q: int, status_col: int, px: float, py: float, pz: float):
+    """Monte Carlo depolarizing channel on qubit q (PAPER.md:652-700 unitary_kraus with an
+    external status): theta column `status_col` of each row holds its status x in [0, 1);
+    the payload carries (px, py, pz)."""
+    return c.add("depol", q, param=status_col, coeff=1.0,
+                 matrix=np.array([px + 1j * py, pz + 0j], dtype=np.complex128))
+
+
+def noisy_vqe(n: int, d: int, px: float = 0.2, py: float = 0.2, pz: float = 0.2) -> Circuit:
+    """PAPER.md:1149-1174 shape: a C6 ansatz layer structure with a depolarizing channel on
+    every qubit after each layer; parameters = 3 n d weights, then n d status columns."""
+    base = hea(n, d)
+    c = Circuit(n, 3 * n * d + n * d)
+    per_layer = len(base.gates) // d
+    for l in range(d):
+        c.gates.extend(base.gates[l * per_layer:(l + 1) * per_layer])
+        for q in range(n):
+            add_depolarizing(c, q, 3 * n * d + l * n + q, px, py, pz)
+    return c
+
+
+def statuses(B: int, n_cols: int, seed: int) -> np.ndarray:
+    """Uniform [0, 1) statuses (PAPER.md:1170 implicit_randu), numpy PCG64 seeded."""
+    return np.random.default_rng(seed).uniform(0.0, 1.0, size=(B, n_cols))
+
+
 def random_unitary(dim: int, rng) -> np.ndarray:
     z = rng.normal(size=(dim, dim)) + 1j * rng.normal(size=(dim, dim))
     q, r = np.linalg.qr(z)
