@@ -1117,6 +1117,14 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
 
   // ---- stages, kernel tables, matrix and accumulator layout
   int mat = 0, acc = 0;
+  // Adjoint shortcut: the reverse sweep needs psi and lambda only through quantities that
+  // are invariant under the same unitary applied to both on bits no later-processed op
+  // touches (partial traces over those bits, inner products).  So an op that no earlier op
+  // (in execution order) touches -- e.g. the first rotation layer -- takes its gradient
+  // term in the backward but skips U^dagger on psi and lambda.  Execution order = passes,
+  // stages, ops as emitted below; off for sharded plans (exchanges move data across bits).
+  uint64_t touched_exec = 0;
+  static const bool no_skip = getenv("TCX_NO_UDAG_SKIP") != nullptr;
   for (auto& pass : P.passes) {
     std::vector<StageOut> stages;
     schedule_stages(P, pass, stages);
@@ -1161,6 +1169,9 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
         KOp ko;
         std::memset(&ko, 0, sizeof(ko));
         ko.type = o.type;
+        o.skip_udag = !no_skip && gb == 0 && (o.type == OP_U1 || o.type == OP_DIAG) &&
+                      (o.bits & touched_exec) == 0;
+        touched_exec |= o.bits;
         ko.acc = -1;
         ko.term = -1;
         o.mat_off = mat;
@@ -1169,6 +1180,7 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
         if (o.type == OP_U1) {
           ko.a = (uint8_t)slot_of(o.b0);
           ko.nterm = (int16_t)u1_class_of(o.cons);
+          ko.cbit = o.skip_udag ? 1 : 0;  // U1 / DIAG: backward skips U^dagger
         } else if (o.type == OP_U2F) {  // tile-local positions (shared-memory op)
           ko.a = (uint8_t)loc[o.b0];
           ko.b = (uint8_t)loc[o.b1];
@@ -1187,6 +1199,7 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
           ko.nterm = (int16_t)o.terms.size();
           ko.term = (int)P.kterms.size() - pass.kterm_begin;
           ko.a = o.lut ? 1 : 0;  // JIT: table-driven phase (one weight class)
+          ko.cbit = o.skip_udag ? 1 : 0;
           {
             std::set<uint32_t> rm;  // register-slot masks (the kernels' phase groups)
             for (auto& tm : o.terms) {

@@ -50,6 +50,8 @@ struct Op {
   std::vector<DiagTerm> terms;    // DIAG
   int nslots = 0;                 // DIAG: distinct gradient slots
   bool has_param = false;
+  bool skip_udag = false;  // backward: no op executed before it touches its bits, so U^dagger
+                           // on psi and lambda can be skipped (plan.cpp, stage emission)
   bool lut = false;  // DIAG: one weight class (param, |w|); phase from a (T+1)-entry table
   int ngroups = 0;   // DIAG (not LUT): distinct register-slot masks of its terms = complex
                      // multiplies per amplitude in the kernels (cost model)

@@ -605,18 +605,20 @@ double op_flops(const Op& o, bool bwd) {
   for (auto& t : o.terms) npar += t.param >= 0;
   switch (o.type) {
     case OP_U1:
-      // gradient: 3 Pauli components of R' = 12 FMA per pair (one component: 4)
+      // gradient: 3 Pauli components of R' = 12 FMA per pair (one component: 4); ops no
+      // earlier op touches skip U^dagger in the backward (plan.cpp skip_udag)
       if (u1_class(o.cons))  // structured: real scalar x complex terms
-        return bwd ? 12.0 + (o.has_param ? 4.0 : 0.0) : 6.0;
-      return bwd ? 28.0 + (o.has_param ? 12.0 : 0.0) : 14.0;
+        return bwd ? (o.skip_udag ? 0.0 : 12.0) + (o.has_param ? 4.0 : 0.0) : 6.0;
+      return bwd ? (o.skip_udag ? 0.0 : 28.0) + (o.has_param ? 12.0 : 0.0) : 14.0;
     case OP_U2F: return bwd ? 60.0 : 30.0;
     case OP_CX: return 0.0;
     default:
       // one complex multiply per amplitude per phase group (LUT: one table entry); the
       // backward conjugate-multiplies psi and lambda and accumulates Im(lambda* psi) terms
-      if (o.lut) return bwd ? 12.0 + (o.has_param ? 4.0 : 0.0) : 6.0;
+      if (o.lut) return bwd ? (o.skip_udag ? 0.0 : 12.0) + (o.has_param ? 4.0 : 0.0) : 6.0;
       (void)nt;
-      return bwd ? 12.0 * std::max(o.ngroups, 1) + 2.0 * npar : 6.0 * std::max(o.ngroups, 1);
+      return bwd ? (o.skip_udag ? 0.0 : 12.0 * std::max(o.ngroups, 1)) + 2.0 * npar
+                 : 6.0 * std::max(o.ngroups, 1);
   }
 }
 double pass_flops(const Plan& P, const PassInfo& p, bool bwd) {
