@@ -352,3 +352,20 @@ def test_workspace_too_small(tc):
     rc = tc._lib.tcx_grad_batch(C.h, P.h, ctypes.c_void_p(th.data_ptr()), 1, ctypes.c_void_p(E.data_ptr()),
                                 ctypes.c_void_p(G.data_ptr()), ctypes.c_void_p(buf.data_ptr()), 64, None)
     assert rc == 1 and "workspace too small" in tc.last_error()
+
+
+@pytest.mark.parametrize("opts", [{}, {"dense_k": 2}])
+def test_batch_above_grid_y_limit(tc, opts):
+    """B = 70000 > 65535 rows: launches are chunked over grid.y; sampled rows (both sides of
+    the chunk boundary) against the oracle, per-term values as well."""
+    n, B = 4, 70000
+    c, H = W.hea(n, 2), W.heisenberg(n)
+    th = W.thetas(B, c.n_params, 70)
+    C, P = tc.Circuit(c, "c128", **opts), tc.Pauli(H)
+    E, G = tc.grad_batch(C, P, _th(th))
+    rows = [0, 65534, 65535, 65536, B - 1]
+    Er, Gr = orc.value_grad_batch(c, H, th[rows])
+    check_E(E.cpu().numpy()[rows], Er, H, "c128")
+    check_grad(G.cpu().numpy()[rows], Gr, H, c, "c128")
+    Et = tc.expect_terms_batch(C, P, _th(th)).cpu().numpy()
+    assert np.abs((Et * H.weights).sum(1) - E.cpu().numpy()).max() <= 1e-11 * H.l1
