@@ -90,6 +90,8 @@ struct PassArgs {
   int64_t b0;
   uint64_t init_hmask;     // M_INIT: leading H gates folded into the initial state |+> on
   double init_amp;         //   these bits, amplitude init_amp = 2^(-popc/2) (plan.cpp)
+  int fold_active;         // 1: the call starts from |0..0>, so leading U1 ops folded into
+                           //   the product initial state are skipped in forward passes (JIT)
 };
 
 struct SmemLayout {

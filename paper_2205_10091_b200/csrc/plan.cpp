@@ -63,10 +63,21 @@ struct Lowerer {
   Run runs[kMaxQubits];
   int last_on_bit[kMaxQubits];
   int last_diag = -1;
-  explicit Lowerer(Plan& p) : P(p) { std::fill(last_on_bit, last_on_bit + kMaxQubits, -1); }
+  bool fold = false;              // fold leading U1 ops into the product initial state
+  bool pristine[kMaxQubits];      // physical bit still |0> (no op emitted, not H-folded)
+  explicit Lowerer(Plan& p) : P(p) {
+    std::fill(last_on_bit, last_on_bit + kMaxQubits, -1);
+    std::fill(pristine, pristine + kMaxQubits, true);
+  }
 
   void emit(Op&& op) {
     int idx = (int)P.ops.size();
+    if (fold && op.type == OP_U1 && pristine[op.b0]) {
+      op.fold_init = true;
+      P.fold_mask |= 1ull << op.b0;
+    }
+    for (int b = 0; b < P.n; ++b)
+      if (op.bits >> b & 1) pristine[b] = false;
     for (int b = 0; b < P.n; ++b)
       if (op.bits >> b & 1) last_on_bit[b] = idx;
     if (op.type == OP_DIAG) last_diag = idx;
@@ -887,11 +898,16 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
   // QAOA's H^n layer (PAPER.md:391 default input, SURVEY §8d cfg3 "H layer folded into a
   // write-only init").  The _in entries (caller input states) apply them explicitly.
   static const bool hfold = getenv("TCX_NO_HFOLD") == nullptr;
+  // Leading U1 runs on |0> bits fold into a product initial state in the JIT's first pass
+  // (the op stays in the plan for the backward's gradient term; with caller input states
+  // the forward applies it as usual): amplitude(r) = prod over folded bits b of U_b[r_b][0].
+  L.fold = gb == 0 && getenv("TCX_NO_UFOLD") == nullptr;
   std::vector<char> touched(n, 0);
   for (int64_t g = 0; g < G && P.dense_k == 0; ++g) {
     const tcx_gate& x = gates[g];
     if (hfold && x.kind == TCX_H && !touched[x.q0]) {
       P.init_hmask |= 1ull << pos[x.q0];
+      L.pristine[pos[x.q0]] = false;
       touched[x.q0] = 1;
       continue;
     }
@@ -1181,6 +1197,7 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
           ko.a = (uint8_t)slot_of(o.b0);
           ko.nterm = (int16_t)u1_class_of(o.cons);
           ko.cbit = o.skip_udag ? 1 : 0;  // U1 / DIAG: backward skips U^dagger
+          ko.b = o.fold_init ? 1 : 0;      // U1: folded into the first pass's initial state
         } else if (o.type == OP_U2F) {  // tile-local positions (shared-memory op)
           ko.a = (uint8_t)loc[o.b0];
           ko.b = (uint8_t)loc[o.b1];

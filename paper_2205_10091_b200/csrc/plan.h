@@ -50,6 +50,8 @@ struct Op {
   std::vector<DiagTerm> terms;    // DIAG
   int nslots = 0;                 // DIAG: distinct gradient slots
   bool has_param = false;
+  bool fold_init = false;  // U1: the first op on a |0> bit; the JIT's first pass writes the
+                           // product state it produces (column 0 of its 2x2 per theta row)
   bool skip_udag = false;  // backward: no op executed before it touches its bits, so U^dagger
                            // on psi and lambda can be skipped (plan.cpp, stage emission)
   bool lut = false;  // DIAG: one weight class (param, |w|); phase from a (T+1)-entry table
@@ -187,6 +189,7 @@ struct Plan {
   int jit_nsub = 1;              // lock-stepped sub-tiles per CTA in JIT kernels
 
   uint64_t init_hmask = 0;         // leading H gates folded into the initial state (bits)
+  uint64_t fold_mask = 0;          // bits whose leading U1 op is folded into the initial state
   double init_amp = 1.0;           // 2^(-popc(init_hmask)/2)
   int dense_k = 0;                 // > 0: gates run as dense k-qubit blocks (tcx_build_opts)
   std::vector<DBlock> dblocks;     // in execution order (before the window passes)

@@ -605,6 +605,7 @@ double op_flops(const Op& o, bool bwd) {
   for (auto& t : o.terms) npar += t.param >= 0;
   switch (o.type) {
     case OP_U1:
+      if (!bwd && o.fold_init) return 0.0;  // written by the first pass's product init
       // gradient: 3 Pauli components of R' = 12 FMA per pair (one component: 4); ops no
       // earlier op touches skip U^dagger in the backward (plan.cpp skip_udag)
       if (u1_class(o.cons))  // structured: real scalar x complex terms
@@ -877,6 +878,7 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
     a.last_is_top = 1;
     a.init_hmask = P.init_hmask;
     a.init_amp = P.init_amp;
+    a.fold_active = psi0 ? 0 : 1;
   };
   auto set_pass = [&](PassArgs& a, const PassInfo& p, bool with_ops) {
     a.stages = (const KStage*)DT->kstages.p + p.stage_begin;
