@@ -839,7 +839,9 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
   int c = opts && opts->coalesce_bits > 0 ? opts->coalesce_bits : (c128 ? 2 : 3);
   t = std::min(t, kMaxTileBits);
   if (t >= n - gb) t = n - gb;
-  int r = opts && opts->reg_bits > 0 ? opts->reg_bits : (t < tdef ? 3 : 4);
+  // register bits per stage: 4 for full tiles; small single-tile states use more threads per
+  // tile (latency-bound: cfg1 n=10 c128 measured 255k -> 287k circuits/s with r = 2)
+  int r = opts && opts->reg_bits > 0 ? opts->reg_bits : (t < tdef ? (n - gb <= 10 ? 2 : 3) : 4);
   r = std::min(r, kMaxRegBits);
   if (r > t) r = t;
   if (t - r > 9) r = t - 9;  // at most 512 threads per tile (kernel launch bounds)
