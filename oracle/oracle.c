@@ -339,11 +339,14 @@ static double energy(int n, int G, const int *kind, const int *q0, const int *q1
  *   psi <- U_g^dag psi; lambda <- U_g^dag lambda.
  * (d/da <psi|H|psi> with U = exp(-i a P/2) gives 2 Re <lambda|(-i/2) P|psi> = Im<lambda|P|psi>.)
  * E[0] = Re <psi|H|psi>, E[1] = Im (must be ~0). */
+/* qim (optional, [P]): Im <psi|H|d psi / d theta_p>, the imaginary
+ * part of the quantity whose real part is grad / 2: with psi = V U_g(a) W |psi0> and
+ * dU_g/da = (-i/2) P_g U_g, <psi|H|d psi/da> = (-i/2) <lambda|P_g|psi> at gate g. */
 static int value_grad_c(int n, int G, const int *kind, const int *q0, const int *q1,
                         const int *param, const double *coeff, const int64_t *moff,
                         const double *mats, int P, const double *theta,
                         int T, const unsigned char *codes, const double *w,
-                        double *E, double *grad, const cplx *psi0)
+                        double *E, double *grad, const cplx *psi0, double *qim)
 {
     const int64_t N = (int64_t)1 << n;
     cplx *psi = malloc(sizeof(cplx) * N), *lam = malloc(sizeof(cplx) * N);
@@ -355,13 +358,17 @@ static int value_grad_c(int n, int G, const int *kind, const int *q0, const int 
     E[0] = creal(e);
     E[1] = cimag(e);
     for (int p = 0; p < P; ++p) grad[p] = 0;
+    if (qim)
+        for (int p = 0; p < P; ++p) qim[p] = 0;
     for (int g = G - 1; g >= 0; --g) {
         if (is_rotation(kind[g]) && param[g] >= 0) {
             cplx gen[16];
             generator(kind[g], gen);
             memcpy(tmp, psi, sizeof(cplx) * N);
             apply_matrix(n, tmp, kind[g], q0[g], q1[g], gen);
-            grad[param[g]] += coeff[g] * cimag(inner(N, lam, tmp));
+            const cplx z = inner(N, lam, tmp);       /* <lambda|P_g|psi> */
+            grad[param[g]] += coeff[g] * cimag(z);  /* 2 Re((-i/2) z) */
+            if (qim) qim[param[g]] += -0.5 * coeff[g] * creal(z);
         }
         cplx m[16], md[16];
         double a = gate_arg(g, kind, param, coeff, theta, -1, 0.0);
@@ -381,7 +388,17 @@ int orc_value_grad(int n, int G, const int *kind, const int *q0, const int *q1,
                    double *E, double *grad)
 {
     return value_grad_c(n, G, kind, q0, q1, param, coeff, moff, mats, P, theta, T, codes, w,
-                        E, grad, NULL);
+                        E, grad, NULL, NULL);
+}
+
+int orc_value_qgrad(int n, int G, const int *kind, const int *q0, const int *q1,
+                    const int *param, const double *coeff, const int64_t *moff,
+                    const double *mats, int P, const double *theta,
+                    int T, const unsigned char *codes, const double *w,
+                    double *E, double *grad, double *qim)
+{
+    return value_grad_c(n, G, kind, q0, q1, param, coeff, moff, mats, P, theta, T, codes, w,
+                        E, grad, NULL, qim);
 }
 
 /* ---------------------------------------------------- parameter shift */
@@ -429,7 +446,7 @@ static int value_grad_batch_c(int n, int G, const int *kind, const int *q0, cons
         err |= value_grad_c(n, G, kind, q0, q1, param, coeff, moff, mats, P,
                             theta + (int64_t)b * P, T, codes, w, E + 2 * b,
                             grad + (int64_t)b * P,
-                            psi0 ? (const cplx *)(psi0 + 2 * N * b) : NULL) != 0;
+                            psi0 ? (const cplx *)(psi0 + 2 * N * b) : NULL, NULL) != 0;
     (void)nthreads;
     return err ? -2 : 0;
 }

@@ -142,6 +142,24 @@ def value_grad(circ, H, theta):
     return E[0], E[1], grad[:circ.n_params]
 
 
+def value_qgrad(circ, H, theta):
+    """(E, grad[P], qim[P]): qim_p = Im <psi|H|d psi/d theta_p>."""
+    g = _Gates(circ)
+    th = np.ascontiguousarray(np.asarray(theta, dtype=np.float64).reshape(-1))
+    if th.size == 0:
+        th = np.zeros(1)
+    codes, w = _ham(H)
+    E = np.zeros(2)
+    grad = np.zeros(max(circ.n_params, 1))
+    qim = np.zeros(max(circ.n_params, 1))
+    rc = lib().orc_value_qgrad(*g.args, ctypes.c_int(circ.n_params), _p(th, ctypes.c_double),
+                               ctypes.c_int(len(w)), _p(codes, ctypes.c_ubyte),
+                               _p(w, ctypes.c_double), _p(E, ctypes.c_double),
+                               _p(grad, ctypes.c_double), _p(qim, ctypes.c_double))
+    assert rc == 0
+    return E[0], grad[:circ.n_params], qim[:circ.n_params]
+
+
 def param_shift(circ, H, theta):
     g = _Gates(circ)
     th = np.ascontiguousarray(np.asarray(theta, dtype=np.float64).reshape(-1))

@@ -435,3 +435,35 @@ def test_noisy_vqe_gradient_per_trajectory():
     ps = orc.param_shift(c, H, th)
     np.testing.assert_allclose(g, ps, atol=1e-10)
     assert np.all(g[3 * n * d:] == 0.0)
+
+
+# --------------------------- <psi|H|d psi>
+def test_psi_h_dpsi_closed_forms():
+    """Rx(t)|0>: <psi|Z|d psi> = -sin(t)/2 (real: half of dE/dt), <psi|X|d psi> = -i/2 for
+    every t (E = 0 identically, the imaginary part is not)."""
+    for t in (0.3, 1.1, -2.0):
+        c = W.Circuit(1, 1).add("rx", 0, param=0, coeff=1.0)
+        _, g, qi = orc.value_qgrad(c, W.pauli_sum(1, [({0: "Z"}, 1.0)]), np.array([t]))
+        assert abs(g[0] / 2 + np.sin(t) / 2) < 1e-14 and abs(qi[0]) < 1e-14
+        _, g, qi = orc.value_qgrad(c, W.pauli_sum(1, [({0: "X"}, 1.0)]), np.array([t]))
+        assert abs(g[0]) < 1e-14 and abs(qi[0] + 0.5) < 1e-14
+
+
+def test_psi_h_dpsi_finite_difference():
+    """Im <psi|H|d psi/d theta_p> against central differences of the state (h = 1e-5), on a
+    random circuit with shared parameters and every rotation kind."""
+    n = 4
+    c = W.random_circuit(n, 40, 91, n_params=5, with_payload=True)
+    H = W.random_pauli_sum(n, 6, 9)
+    th = W.thetas(1, 5, 4)[0]
+    _, g, qi = orc.value_qgrad(c, H, th)
+    psi = orc.state(c, th)
+    from oracle import bruteforce
+    Hm = bruteforce.hamiltonian_dense(H)
+    hpsi = Hm @ psi
+    for p in range(5):
+        e = np.zeros(5)
+        e[p] = 1e-5
+        d = (orc.state(c, th + e) - orc.state(c, th - e)) / 2e-5
+        q = np.vdot(hpsi, d)
+        assert abs(q.imag - qi[p]) < 1e-8 and abs(2 * q.real - g[p]) < 1e-8
