@@ -198,6 +198,15 @@ tcx_status tcx_state_batch_in(const tcx_circuit* circ, const double* theta, int6
                               const void* psi0, void* state, void* ws, size_t ws_bytes,
                               void* cuda_stream);
 
+/* <psi|H|d psi/d theta>: its real part is grad / 2, its
+ * imaginary part is written to q_im[b][p] (device [B][n_params] float64); E and grad as in
+ * tcx_grad_batch.  Produced by the dense-block adjoint (which keeps the full 2^k x 2^k
+ * R' = sum psi lambda^dagger): the circuit must be built with dense_k in 1..4, else
+ * TCX_E_UNSUPPORTED.  ws sized with TCX_WS_GRAD. */
+tcx_status tcx_grad_batch_q(const tcx_circuit* circ, const tcx_pauli* pauli,
+                            const double* theta, int64_t B, double* E, double* grad,
+                            double* q_im, void* ws, size_t ws_bytes, void* cuda_stream);
+
 /* Per-term values (vvag over Pauli structures returns
  * f(w, v_j) for every term next to the summed gradient, which is tcx_grad_batch with unit
  * weights): E_terms[b][j] = Re <psi_b|P_j|psi_b> (weights ignored), device [B][n_terms]

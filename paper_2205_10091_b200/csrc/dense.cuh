@@ -420,6 +420,17 @@ __global__ void __launch_bounds__(256) dense_bwd_kernel(const DenseArgs a) {
   }
 }
 
+// qim[b][p] = sum of the q contributions of parameter p (fixed CSR order)
+__global__ void dense_qim_kernel(const double* qcontrib, int ncontrib, const int32_t* pptr,
+                                 const int32_t* plist, int P, double* qim, int64_t b0) {
+  const int64_t b = b0 + blockIdx.y;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  double s = 0.0;
+  for (int i = pptr[p]; i < pptr[p + 1]; ++i) s += qcontrib[(size_t)b * ncontrib + plist[i]];
+  qim[(size_t)b * P + p] = s;
+}
+
 // R'[b][acc_off + e] = sum_s part[b][s][e], fixed order (C10)
 __global__ void dense_rsum_kernel(const double* part, double* rs, int S, int ne, int acc_off,
                                   int acc_total, int64_t b0) {
@@ -444,6 +455,8 @@ struct DenseGradArgs {
   const double* rs;        // [B][acc_total] R' (re, im)
   int acc_total;
   double* contrib;         // [B][ncontrib]
+  double* qcontrib;        // optional [B][ncontrib]: -coeff_g Re Tr(B_g R') / 2, the
+                           //   contributions to Im <psi|H|d psi/d theta>
   int ncontrib;
   int64_t b0;
 };
@@ -453,7 +466,7 @@ __global__ void dense_grad_kernel(const DenseGradArgs a) {
   const int64_t b = a.b0 + blockIdx.y;
   const int D = 1 << blk.k, DD = D * D, tid = threadIdx.x;
   __shared__ cz S[256], T[256];
-  __shared__ double red[256];
+  __shared__ double red[256], red2[256];
   const double* th = a.theta + b * a.P;
   const double* Rp = a.rs + (size_t)b * a.acc_total + blk.acc_off;
   const int i = tid / D, j = tid % D;
@@ -469,7 +482,7 @@ __global__ void dense_grad_kernel(const DenseGradArgs a) {
       if (g.kind == TCX_RY || g.kind == TCX_RYY) ym = sa | sb;
       if (g.kind == TCX_RZ || g.kind == TCX_RZZ) zm = sa | sb;
       xm |= ym;
-      double v = 0.0;
+      double v = 0.0, vr = 0.0;
       if (tid < DD) {
         // (S P)_im = S_{i, m ^ xm} ph(m), P|m> = ph(m) |m ^ xm>,
         // ph(m) = i^{nY} (-1)^{popc(m & (ym | zm))} (Y|0> = i|1>, Y|1> = -i|0>)
@@ -486,13 +499,19 @@ __global__ void dense_grad_kernel(const DenseGradArgs a) {
         // Im(B_ij R'_ji)
         const cz R = {Rp[2 * (j * D + i)], Rp[2 * (j * D + i) + 1]};
         v = Bij.x * R.y + Bij.y * R.x;
+        vr = Bij.x * R.x - Bij.y * R.y;
       }
       red[tid] = v;
+      red2[tid] = vr;
       __syncthreads();
       if (tid == 0) {
-        double s = 0.0;
-        for (int e = 0; e < DD; ++e) s += red[e];
-        a.contrib[(size_t)b * a.ncontrib + g.contrib] = g.coeff * s;
+        double s = 0.0, sr = 0.0;
+        for (int e = 0; e < DD; ++e) {
+          s += red[e];
+          sr += red2[e];
+        }
+        a.contrib[(size_t)b * a.ncontrib + g.contrib] = g.coeff * s;  // 2 Re q = Im Tr(B R')
+        if (a.qcontrib) a.qcontrib[(size_t)b * a.ncontrib + g.contrib] = -0.5 * g.coeff * sr;
       }
       __syncthreads();
     }

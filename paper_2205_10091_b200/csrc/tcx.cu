@@ -531,7 +531,7 @@ enum { K_EXPECT = 0, K_GRAD = 1, K_STATE = 2 };
 
 struct WsLayout {
   size_t psi, lam, mats, part, epart, tot, contrib, theta, E, grad, total;
-  size_t dmats, dshared, dpart, drs;  // dense blocks: U tables, R' partials / sums
+  size_t dmats, dshared, dpart, drs, dq;  // dense blocks: U tables, R' partials / sums, q
   bool mega;
 };
 
@@ -577,6 +577,7 @@ WsLayout ws_layout(const Plan& P, const Binding* Bd, int64_t B, int kind, bool h
       const int k = dense_max_k(P);
       w.dpart = take((size_t)B * dense_bwd_ctas(P) * 2 * (1 << (2 * k)) * 8);
       w.drs = take((size_t)B * P.dacc_total * 8);
+      w.dq = take((size_t)B * std::max(P.n_contrib, 1) * 8);
     }
   }
   if (host_io) {
@@ -730,7 +731,7 @@ struct OneStep {
 tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, double* E,
                double* grad, void* state, void* ws, size_t ws_bytes, cudaStream_t st, int kind,
                const WsLayout* wl_in, const OneStep* one = nullptr, const void* psi0 = nullptr,
-               bool keep_state = false) {
+               bool keep_state = false, double* qim = nullptr) {
   if (P.gbits > 0 && !one)
     return fail(TCX_E_INVALID, "sharded circuit (global_bits > 0): use tcx_shard_program/exec");
   auto want = [&](int k, int a) { return !one || (one->kind == k && one->arg == a); };
@@ -1132,11 +1133,20 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
       g.rs = (const double*)(W + wl.drs);
       g.acc_total = P.dacc_total;
       g.contrib = (double*)(W + wl.contrib);
+      g.qcontrib = qim ? (double*)(W + wl.dq) : nullptr;
       g.ncontrib = std::max(P.n_contrib, 1);
       g.b0 = b0;
       dense_grad_kernel<<<dim3(npb, (unsigned)rows), 256, 0, st>>>(g);
       CUDA_TRY(cudaGetLastError());
+      if (qim && P.P > 0) {
+        dense_qim_kernel<<<dim3((P.P + 127) / 128, (unsigned)rows), 128, 0, st>>>(
+            g.qcontrib, g.ncontrib, (const int32_t*)DT->pptr.p, (const int32_t*)DT->plist.p, P.P,
+            qim, b0);
+        CUDA_TRY(cudaGetLastError());
+      }
     }
+  } else if (qim && P.P > 0) {
+    CUDA_TRY(cudaMemsetAsync(qim, 0, sizeof(double) * (size_t)B * P.P, st));  // no parameters
   }
   // ---- finalize / export
   if (kind != K_STATE) {
@@ -1298,6 +1308,19 @@ tcx_status tcx_state_batch(const tcx_circuit* circ, const double* theta, int64_t
   if (!circ) return fail(TCX_E_INVALID, "null circuit");
   return run(const_cast<tcx_circuit*>(circ)->plan, nullptr, theta, B, nullptr, nullptr, state,
              ws, ws_bytes, (cudaStream_t)stream, K_STATE, nullptr);
+}
+
+tcx_status tcx_grad_batch_q(const tcx_circuit* circ, const tcx_pauli* pauli, const double* theta,
+                            int64_t B, double* E, double* grad, double* q_im, void* ws,
+                            size_t ws_bytes, void* stream) {
+  g_err.clear();
+  if (!circ || !q_im) return fail(TCX_E_INVALID, "null circuit or q_im");
+  Plan& P = const_cast<tcx_circuit*>(circ)->plan;
+  if (P.dblocks.empty())
+    return fail(TCX_E_UNSUPPORTED,
+                "Im <psi|H|d psi> is produced by the dense-block adjoint: build with dense_k in 1..4");
+  return run(P, pauli, theta, B, E, grad, nullptr, ws, ws_bytes, (cudaStream_t)stream, K_GRAD,
+             nullptr, nullptr, nullptr, false, q_im);
 }
 
 tcx_status tcx_expect_batch_in(const tcx_circuit* circ, const tcx_pauli* pauli,

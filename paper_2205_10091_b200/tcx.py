@@ -89,6 +89,7 @@ _sig = {
     "tcx_grad_batch_in": [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _sz, _vp],
     "tcx_state_batch_in": [_vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp],
     "tcx_expect_terms_batch": [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp],
+    "tcx_grad_batch_q": [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _sz, _vp],
     "tcx_expect_batch_host": [_vp, _vp, _vp, _i64, _vp, _vp, _sz, _vp],
     "tcx_grad_batch_host": [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp],
     "tcx_circuit_info": [_vp, _vp, ctypes.POINTER(tcx_plan_info)],
@@ -349,6 +350,24 @@ def state_batch(circ: Circuit, theta, stream=None, ws: Workspace = None, psi0=No
                                 ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(buf.data_ptr()),
                                 buf.numel(), _stream_ptr(stream)))
     return out
+
+
+def grad_batch_q(circ: Circuit, pauli: Pauli, theta, stream=None, ws: Workspace = None):
+    """(E [B], grad [B, P], q_im [B, P]) with q_im = Im <psi|H|d psi/d theta> and
+    grad = 2 Re of the same quantity (tcx_grad_batch_q; dense plans)."""
+    torch = _torch()
+    theta = theta.contiguous()
+    assert theta.dtype == torch.float64 and theta.is_cuda
+    B = theta.shape[0]
+    E = torch.empty(B, dtype=torch.float64, device=theta.device)
+    G = torch.empty(B, max(circ.P, 1), dtype=torch.float64, device=theta.device)
+    Q = torch.empty(B, max(circ.P, 1), dtype=torch.float64, device=theta.device)
+    buf, need = (ws or _default_ws).get(circ, pauli, B, WS_GRAD, theta.device)
+    _check(_lib.tcx_grad_batch_q(circ.h, pauli.h, ctypes.c_void_p(theta.data_ptr()), B,
+                                 ctypes.c_void_p(E.data_ptr()), ctypes.c_void_p(G.data_ptr()),
+                                 ctypes.c_void_p(Q.data_ptr()), ctypes.c_void_p(buf.data_ptr()),
+                                 buf.numel(), _stream_ptr(stream)))
+    return E, G[:, :circ.P], Q[:, :circ.P]
 
 
 def expect_terms_batch(circ: Circuit, pauli: Pauli, theta, stream=None, ws: Workspace = None,

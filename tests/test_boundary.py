@@ -212,3 +212,18 @@ def test_h_fold_follows_swap_relabels():
     from paper_2205_10091_b200 import tcx as m
     c = W.Circuit(3, 1).add("rx", 0, param=0, coeff=1.0).add("swap", 0, 1).add("h", 1).add("h", 0)
     assert m.Circuit(c, "c64").info()["init_h"] == 1
+
+
+def test_psi_h_dpsi_needs_dense_plan():
+    """tcx_grad_batch_q is produced by the dense adjoint: window plans say so (before any
+    device work)."""
+    from paper_2205_10091_b200 import tcx as m
+    c = W.hea(4, 1)
+    C, P = m.Circuit(c, "c64"), m.Pauli(W.tfim_zz_x(4))
+    buf = ctypes.create_string_buffer(1 << 12)
+    x = np.zeros(64)
+    rc = m._lib.tcx_grad_batch_q(C.h, P.h, ctypes.c_void_p(x.ctypes.data), 1,
+                                 ctypes.c_void_p(x.ctypes.data), ctypes.c_void_p(x.ctypes.data),
+                                 ctypes.c_void_p(x.ctypes.data), ctypes.cast(buf, ctypes.c_void_p),
+                                 len(buf), None)
+    assert rc == 2 and "dense_k" in m.last_error()

@@ -157,3 +157,20 @@ def test_dense_k5_c64_tensor_core_pair_modes(tc, low):
     ref = orc.state(c, np.zeros(0))
     for b in range(2):
         assert np.abs(psi[b] - ref).max() <= state_tol("c64", len(c.gates))
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("k", [1, 2, 4])
+def test_psi_h_dpsi_dense(tc, dtype, k):
+    """Im <psi|H|d psi/d theta> from the dense adjoint's full R' vs the
+    oracle; its real part (grad / 2) as in tcx_grad_batch."""
+    n = 9
+    c = W.random_circuit(n, 70, 7100 + k, n_params=6, with_payload=True)
+    H = W.random_pauli_sum(n, 8, 71)
+    th = W.thetas(3, 6, k)
+    C, P = tc.Circuit(c, dtype, dense_k=k), tc.Pauli(H)
+    E, G, Q = tc.grad_batch_q(C, P, _th(th))
+    ref = [orc.value_qgrad(c, H, th[b]) for b in range(3)]
+    check_E(E.cpu().numpy(), np.array([r[0] for r in ref]), H, dtype)
+    check_grad(G.cpu().numpy(), np.array([r[1] for r in ref]), H, c, dtype)
+    check_grad(2 * Q.cpu().numpy(), 2 * np.array([r[2] for r in ref]), H, c, dtype, "q_im")
