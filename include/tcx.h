@@ -75,6 +75,12 @@ typedef enum {
      * in the paper's Kraus order I, X, Y, Z: x < 1-px-py-pz -> I, < 1-py-pz -> X, < 1-pz -> Y,
      * else Z.  Not differentiable: its status column gets no gradient contribution. */
     TCX_DEPOL,
+    /* Random-axis rotation (Table VII "vmap over circuit structures":
+     * unitary_kraus over [Rx, Ry, Rz] with probabilities 1/3 and an external status): 1 qubit,
+     * angle = coeff * theta[param] as for rotations, payload = 1 complex element whose real
+     * part is the index s of the theta column holding the row's status x in [0, 1);
+     * x < 1/3 -> R_X, x < 2/3 -> R_Y, else R_Z.  Differentiable in the angle. */
+    TCX_RROT,
     TCX_NKINDS
 } tcx_gate_kind;
 

@@ -41,7 +41,7 @@ enum {
     OK_I = 0, OK_X, OK_Y, OK_Z, OK_H, OK_S, OK_SDG, OK_T, OK_TDG,
     OK_CNOT, OK_CZ, OK_SWAP,
     OK_RX, OK_RY, OK_RZ, OK_RXX, OK_RYY, OK_RZZ,
-    OK_U1, OK_U2, OK_DEPOL, OK_NKINDS
+    OK_U1, OK_U2, OK_DEPOL, OK_RROT, OK_NKINDS
 };
 
 /* ---------------------------------------------------------------- matrices */
@@ -76,7 +76,19 @@ static int arity(int kind)
 static int is_rotation(int kind)
 {
     return kind == OK_RX || kind == OK_RY || kind == OK_RZ ||
-           kind == OK_RXX || kind == OK_RYY || kind == OK_RZZ;
+           kind == OK_RXX || kind == OK_RYY || kind == OK_RZZ || kind == OK_RROT;
+}
+
+/* The gate actually applied by gate g for this theta row: a random-axis rotation
+ * (PAPER.md:1693-1704 unitary_kraus over [Rx, Ry, Rz], probabilities 1/3, external status)
+ * becomes Rx / Ry / Rz by the row's status x = theta[s] (s = the payload's real part):
+ * x < 1/3, x < 2/3, else. */
+static int row_kind(int g, const int *kind, const int64_t *moff, const double *mats,
+                    const double *theta)
+{
+    if (kind[g] != OK_RROT) return kind[g];
+    const double x = theta[(int)mats[2 * moff[g]]];
+    return x < 1.0 / 3.0 ? OK_RX : (x < 2.0 / 3.0 ? OK_RY : OK_RZ);
 }
 
 /* Pauli generator of a rotation gate: P with R_P(a) = exp(-i a P/2). */
@@ -209,6 +221,7 @@ int orc_validate(int n, int G, const int *kind, const int *q0, const int *q1,
         if (is_rotation(k) && (param[g] < -1 || param[g] >= P)) return 1 + g;
         if (k == OK_DEPOL && (param[g] < 0 || param[g] >= P || moff[g] < 0 || moff[g] + 2 > nmat))
             return 1 + g;
+        if (k == OK_RROT && (moff[g] < 0 || moff[g] + 1 > nmat)) return 1 + g;
         if (k == OK_U1 || k == OK_U2) {
             int64_t need = (k == OK_U1 ? 4 : 16);
             if (moff[g] < 0 || moff[g] + need > nmat) return 1 + g;
@@ -253,8 +266,9 @@ static void state_c(int n, int G, const int *kind, const int *q0, const int *q1,
     for (int g = 0; g < G; ++g) {
         cplx m[16];
         double a = gate_arg(g, kind, param, coeff, theta, shift_gate, shift);
-        gate_matrix(kind[g], a, moff[g] >= 0 ? mats + 2 * moff[g] : NULL, m);
-        apply_matrix(n, psi, kind[g], q0[g], q1[g], m);
+        const int k = row_kind(g, kind, moff, mats, theta);
+        gate_matrix(k, a, moff[g] >= 0 ? mats + 2 * moff[g] : NULL, m);
+        apply_matrix(n, psi, k, q0[g], q1[g], m);
     }
 }
 
@@ -361,21 +375,22 @@ static int value_grad_c(int n, int G, const int *kind, const int *q0, const int 
     if (qim)
         for (int p = 0; p < P; ++p) qim[p] = 0;
     for (int g = G - 1; g >= 0; --g) {
+        const int k = row_kind(g, kind, moff, mats, theta);
         if (is_rotation(kind[g]) && param[g] >= 0) {
             cplx gen[16];
-            generator(kind[g], gen);
+            generator(k, gen);
             memcpy(tmp, psi, sizeof(cplx) * N);
-            apply_matrix(n, tmp, kind[g], q0[g], q1[g], gen);
+            apply_matrix(n, tmp, k, q0[g], q1[g], gen);
             const cplx z = inner(N, lam, tmp);       /* <lambda|P_g|psi> */
             grad[param[g]] += coeff[g] * cimag(z);  /* 2 Re((-i/2) z) */
             if (qim) qim[param[g]] += -0.5 * coeff[g] * creal(z);
         }
         cplx m[16], md[16];
         double a = gate_arg(g, kind, param, coeff, theta, -1, 0.0);
-        gate_matrix(kind[g], a, moff[g] >= 0 ? mats + 2 * moff[g] : NULL, m);
-        dagger(m, arity(kind[g]) == 1 ? 2 : 4, md);
-        apply_matrix(n, psi, kind[g], q0[g], q1[g], md);
-        apply_matrix(n, lam, kind[g], q0[g], q1[g], md);
+        gate_matrix(k, a, moff[g] >= 0 ? mats + 2 * moff[g] : NULL, m);
+        dagger(m, arity(k) == 1 ? 2 : 4, md);
+        apply_matrix(n, psi, k, q0[g], q1[g], md);
+        apply_matrix(n, lam, k, q0[g], q1[g], md);
     }
     free(psi); free(lam); free(tmp);
     return 0;

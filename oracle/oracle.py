@@ -20,7 +20,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 # the oracle's own enum order (oracle.c OK_*)
 _KIND = {name: i for i, name in enumerate(
     ("i", "x", "y", "z", "h", "s", "sdg", "t", "tdg", "cnot", "cz", "swap",
-     "rx", "ry", "rz", "rxx", "ryy", "rzz", "u1", "u2", "depol"))}
+     "rx", "ry", "rz", "rxx", "ryy", "rzz", "u1", "u2", "depol", "rrot"))}
 
 _lib = None
 

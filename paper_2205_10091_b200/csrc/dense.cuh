@@ -73,7 +73,12 @@ __device__ void dense_gate_matrix(const DGate& g, const double* th, const double
   const int d = g.b >= 0 ? 4 : 2;
   for (int i = 0; i < d * d; ++i) m[i] = {0, 0};
   for (int i = 0; i < d; ++i) m[i * d + i] = {1, 0};
-  switch (g.kind) {
+  int kind = g.kind;
+  if (kind == TCX_RROT) {  // axis of this row: status column index in the payload
+    const double x = th[(int)fixed[2 * g.payload]];
+    kind = x < 1.0 / 3.0 ? TCX_RX : (x < 2.0 / 3.0 ? TCX_RY : TCX_RZ);
+  }
+  switch (kind) {
     case TCX_X: m[0] = {0, 0}; m[1] = {1, 0}; m[2] = {1, 0}; m[3] = {0, 0}; break;
     case TCX_Y: m[0] = {0, 0}; m[1] = {0, -1}; m[2] = {0, 1}; m[3] = {0, 0}; break;
     case TCX_Z: m[3] = {-1, 0}; break;
@@ -478,9 +483,14 @@ __global__ void dense_grad_kernel(const DenseGradArgs a) {
       // P_g on local bits (X / Y / Z masks of the rotation generator)
       int xm = 0, ym = 0, zm = 0;
       const int sa = 1 << g.a, sb = g.b >= 0 ? 1 << g.b : 0;
-      if (g.kind == TCX_RX || g.kind == TCX_RXX) xm = sa | sb;
-      if (g.kind == TCX_RY || g.kind == TCX_RYY) ym = sa | sb;
-      if (g.kind == TCX_RZ || g.kind == TCX_RZZ) zm = sa | sb;
+      int gk = g.kind;
+      if (gk == TCX_RROT) {
+        const double x = th[(int)a.fixed[2 * g.payload]];
+        gk = x < 1.0 / 3.0 ? TCX_RX : (x < 2.0 / 3.0 ? TCX_RY : TCX_RZ);
+      }
+      if (gk == TCX_RX || gk == TCX_RXX) xm = sa | sb;
+      if (gk == TCX_RY || gk == TCX_RYY) ym = sa | sb;
+      if (gk == TCX_RZ || gk == TCX_RZZ) zm = sa | sb;
       xm |= ym;
       double v = 0.0, vr = 0.0;
       if (tid < DD) {

@@ -27,7 +27,7 @@ using cd = std::complex<double>;
 
 bool is_rot(int k) {
   return k == TCX_RX || k == TCX_RY || k == TCX_RZ || k == TCX_RXX || k == TCX_RYY ||
-         k == TCX_RZZ;
+         k == TCX_RZZ || k == TCX_RROT;
 }
 bool is_2q(int k) {
   return k == TCX_CNOT || k == TCX_CZ || k == TCX_SWAP || k == TCX_RXX || k == TCX_RYY ||
@@ -694,9 +694,10 @@ void build_dense(Plan& P, const tcx_gate* gates, int64_t G, int* pos,
       if (x.kind == TCX_U1) dg.payload = payload_copy(x.payload, 2);
       if (x.kind == TCX_U2) dg.payload = payload_copy(x.payload, 4);
       if (x.kind == TCX_DEPOL) dg.payload = payload_copy_raw(x.payload, 2);
+      if (x.kind == TCX_RROT) dg.payload = payload_copy_raw(x.payload, 1);
       dg.contrib = -1;
       d.has_param |= dg.param >= 0 && is_rot(x.kind);  // gradient slots
-      theta_dep |= dg.param >= 0;                       // U depends on the theta row
+      theta_dep |= dg.param >= 0 || x.kind == TCX_RROT;  // U depends on the theta row
       P.dgates.push_back(dg);
     }
     d.shared = theta_dep ? 0 : 1;
@@ -816,6 +817,13 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
     } else if (x.param != -1) {
       return bad("param must be -1 for a non-rotation gate");
     }
+    if (x.kind == TCX_RROT) {
+      if (x.payload < 0 || x.payload + 1 > nmat) return bad("payload out of range");
+      const double sc = mats[2 * x.payload];
+      if (!(sc >= 0 && sc < Pn && sc == std::floor(sc)))
+        return bad("random-axis rotation: status column out of range");
+      continue;
+    }
     if (x.kind == TCX_U1 || x.kind == TCX_U2) {
       int64_t need = x.kind == TCX_U1 ? 4 : 16;
       if (x.payload < 0 || x.payload + need > nmat) return bad("payload out of range");
@@ -924,6 +932,7 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
       Constituent cn{x.kind, (is_rot(x.kind) || x.kind == TCX_DEPOL) ? x.param : -1, x.coeff, -1, -1};
       if (x.kind == TCX_U1) cn.payload = payload_copy(x.payload, 2);
       if (x.kind == TCX_DEPOL) cn.payload = payload_copy_raw(x.payload, 2);
+      if (x.kind == TCX_RROT) cn.payload = payload_copy_raw(x.payload, 1);
       L.add1(pos[x.q0], cn, is_diag1(x.kind));
       continue;
     }

@@ -63,6 +63,12 @@ __device__ __forceinline__ cdd cmul(cdd a, cdd b) { return {a.x * b.x - a.y * b.
 __device__ __forceinline__ cdd cadd(cdd a, cdd b) { return {a.x + b.x, a.y + b.y}; }
 __device__ __forceinline__ cdd cconj(cdd a) { return {a.x, -a.y}; }
 
+// TCX_RROT: the rotation axis of this theta row (status column index in the payload)
+__device__ __forceinline__ int rrot_kind(const double* theta, const double* fixed, int64_t payload) {
+  const double x = theta[(int)fixed[2 * payload]];
+  return x < 1.0 / 3.0 ? TCX_RX : (x < 2.0 / 3.0 ? TCX_RY : TCX_RZ);
+}
+
 // 1-qubit gate matrix g[0..3] (row-major) -- same conventions as tcx.h
 __device__ void gate1(const DCons& c, const double* theta, const double* fixed, cdd* g) {
   const double r2 = 0.70710678118654752440;
@@ -70,7 +76,8 @@ __device__ void gate1(const DCons& c, const double* theta, const double* fixed, 
   double cs, sn;
   sincos(0.5 * a, &sn, &cs);
   g[0] = {1, 0}; g[1] = {0, 0}; g[2] = {0, 0}; g[3] = {1, 0};
-  switch (c.kind) {
+  const int kind = c.kind == TCX_RROT ? rrot_kind(theta, fixed, c.payload) : c.kind;
+  switch (kind) {
     case TCX_X: g[0] = {0, 0}; g[1] = {1, 0}; g[2] = {1, 0}; g[3] = {0, 0}; break;
     case TCX_Y: g[0] = {0, 0}; g[1] = {0, -1}; g[2] = {0, 1}; g[3] = {0, 0}; break;
     case TCX_Z: g[3] = {-1, 0}; break;
@@ -225,9 +232,10 @@ __global__ void finalize_kernel(const FinArgs a) {
       const DCons cn = a.cons[g.cons_begin + c];
       if (cn.contrib >= 0) {  // differentiable rotations only (not depolarizing statuses)
         cdd Pm[4] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
-        if (cn.kind == TCX_RX) { Pm[1] = {1, 0}; Pm[2] = {1, 0}; }
-        if (cn.kind == TCX_RY) { Pm[1] = {0, -1}; Pm[2] = {0, 1}; }
-        if (cn.kind == TCX_RZ) { Pm[0] = {1, 0}; Pm[3] = {-1, 0}; }
+        const int ck = cn.kind == TCX_RROT ? rrot_kind(th, a.fixed, cn.payload) : cn.kind;
+        if (ck == TCX_RX) { Pm[1] = {1, 0}; Pm[2] = {1, 0}; }
+        if (ck == TCX_RY) { Pm[1] = {0, -1}; Pm[2] = {0, 1}; }
+        if (ck == TCX_RZ) { Pm[0] = {1, 0}; Pm[3] = {-1, 0}; }
         cdd T1[4], Bm[4], Sd[4] = {cconj(Sfx[0]), cconj(Sfx[2]), cconj(Sfx[1]), cconj(Sfx[3])};
         mat2mul(Sfx, Pm, T1);
         mat2mul(T1, Sd, Bm);

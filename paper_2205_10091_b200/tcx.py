@@ -23,7 +23,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 # tcx_gate_kind (include/tcx.h)
 KIND = {name: i for i, name in enumerate(
     ("i", "x", "y", "z", "h", "s", "sdg", "t", "tdg", "cnot", "cz", "swap",
-     "rx", "ry", "rz", "rxx", "ryy", "rzz", "u1", "u2", "depol"))}
+     "rx", "ry", "rz", "rxx", "ryy", "rzz", "u1", "u2", "depol", "rrot"))}
 C64, C128 = 0, 1
 WS_GRAD, WS_HOST_IO, WS_STATE, WS_INPUTS, WS_TERMS = 1, 2, 4, 8, 16
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_UNSUPPORTED", 3: "E_OOM", 4: "E_CUDA", 5: "E_NCCL"}

@@ -53,3 +53,23 @@ def test_trajectory_average_matches_channel(tc):
     xs = ((np.arange(1000) + 0.5) / 1000)[:, None]
     E = tc.expect_batch(tc.Circuit(c, "c128"), tc.Pauli(W.pauli_sum(1, [({0: "X"}, 1.0)])), _th(xs))
     assert abs(E.cpu().numpy().mean() - (1 - 2 * (0.2 + 0.3))) < 1e-12
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("opts", [{}, {"dense_k": 3}])
+def test_barren_plateau_structures(tc, dtype, opts):
+    """Table VII workload: 100 random structures x weights, 10 qubits,
+    10 layers, vmapped in one batch; E and gradients of every row vs the oracle and the
+    gradient variance over the batch (the quantity the paper benchmarks)."""
+    n, L, B = 10, 10, 100
+    c = W.barren_plateau(n, L)
+    H = W.pauli_sum(n, [({0: "Z", 1: "Z"}, 1.0)])
+    rng = np.random.default_rng(23)
+    th = np.concatenate([rng.uniform(0, 2 * np.pi, (B, n * L)), rng.uniform(0, 1, (B, n * L))], 1)
+    C, P = tc.Circuit(c, dtype, **opts), tc.Pauli(H)
+    E, G = tc.grad_batch(C, P, _th(th))
+    Er, Gr = orc.value_grad_batch(c, H, th, nthreads=os.cpu_count() or 1)
+    check_E(E.cpu().numpy(), Er, H, dtype)
+    check_grad(G.cpu().numpy(), Gr, H, c, dtype)
+    g0, r0 = G.cpu().numpy()[:, 0], Gr[:, 0]
+    assert abs(g0.var() - r0.var()) <= 1e-5 * max(r0.var(), 1e-12) + 1e-10

@@ -467,3 +467,31 @@ def test_psi_h_dpsi_finite_difference():
         d = (orc.state(c, th + e) - orc.state(c, th - e)) / 2e-5
         q = np.vdot(hpsi, d)
         assert abs(q.imag - qi[p]) < 1e-8 and abs(2 * q.real - g[p]) < 1e-8
+
+
+# --------------------- vmap over circuit structures
+def test_random_axis_rotation_closed_forms():
+    """unitary_kraus([Rx, Ry, Rz], prob 1/3 each, status): on |0>, <X> = 0 / sin t / 0 and
+    <Y> = -sin t / 0 / 0 for statuses in [0,1/3), [1/3,2/3), [2/3,1)."""
+    t = 0.7
+    c = W.Circuit(1, 2)
+    W.add_random_rotation(c, 0, 0, 1)
+    HX, HY = W.pauli_sum(1, [({0: "X"}, 1.0)]), W.pauli_sum(1, [({0: "Y"}, 1.0)])
+    for x, ex, ey in ((0.1, 0.0, -np.sin(t)), (0.5, np.sin(t), 0.0), (0.9, 0.0, 0.0)):
+        th = np.array([[t, x]])
+        assert abs(orc.expect_batch(c, HX, th)[0] - ex) < 1e-14
+        assert abs(orc.expect_batch(c, HY, th)[0] - ey) < 1e-14
+
+
+def test_barren_plateau_gradient_per_structure():
+    """Table VII shape at n = 5, 4 layers: for each sampled structure
+    the adjoint gradient equals the parameter shift; structure columns get no gradient."""
+    n, L = 5, 4
+    c = W.barren_plateau(n, L)
+    H = W.pauli_sum(n, [({0: "Z", 1: "Z"}, 1.0)])
+    rng = np.random.default_rng(17)
+    for _ in range(3):
+        th = np.concatenate([rng.uniform(0, 2 * np.pi, n * L), rng.uniform(0, 1, n * L)])
+        _, _, g = orc.value_grad(c, H, th)
+        np.testing.assert_allclose(g, orc.param_shift(c, H, th), atol=1e-10)
+        assert np.all(g[n * L:] == 0.0)

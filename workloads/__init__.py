@@ -218,6 +218,27 @@ def noisy_vqe(n: int, d: int, px: float = 0.2, py: float = 0.2, pz: float = 0.2)
     return c
 
 
+def add_random_rotation(c: Circuit, q: int, angle_col: int, status_col: int, coeff: float = 1.0):
+    """Random-axis rotation: Rx / Ry / Rz of angle coeff * theta[angle_col]
+    chosen by the row's status theta[status_col] (< 1/3, < 2/3, else); the payload carries the
+    status column index."""
+    return c.add("rrot", q, param=angle_col, coeff=coeff,
+                 matrix=np.array([float(status_col) + 0j], dtype=np.complex128))
+
+
+def barren_plateau(n: int, layers: int) -> Circuit:
+    """Table VII workload: per layer a random-axis rotation on every
+    qubit (weights theta[l n + i], structure statuses theta[n L + l n + i]), then CZ(i, i+1)
+    for i < n-1.  P = 2 n L; each theta row is one (weights, structure) pair."""
+    c = Circuit(n, 2 * n * layers)
+    for l in range(layers):
+        for i in range(n):
+            add_random_rotation(c, i, l * n + i, n * layers + l * n + i)
+        for i in range(n - 1):
+            c.add("cz", i, i + 1)
+    return c
+
+
 def statuses(B: int, n_cols: int, seed: int) -> np.ndarray:
     """Uniform [0, 1) statuses (PAPER.md:1170 implicit_randu), numpy PCG64 seeded."""
     return np.random.default_rng(seed).uniform(0.0, 1.0, size=(B, n_cols))
