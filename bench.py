@@ -148,7 +148,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="tcx", choices=["tcx", "reference"])
-    ap.add_argument("--config", type=int, default=1, help="BASELINE.json configs index")
+    ap.add_argument("--config", type=int, default=1,
+                    help="BASELINE.json configs index (5: the paper's Table VII barren-plateau task)")
     ap.add_argument("--batch", type=int, default=None, help="theta rows per rank")
     ap.add_argument("--batch-qubits", type=int, default=None,
                     help="config 4: local qubits per rank (default 33)")
@@ -197,7 +198,7 @@ def main():
     if args.dtype and args.dtype != dtype:
         name, dtype = name.replace("_" + dtype, "_" + args.dtype), args.dtype
     B = theta.shape[0]
-    if world > 1 and rank > 0:  # distinct seeded rows per rank (weak scaling)
+    if world > 1 and rank > 0 and args.config in (0, 1, 2):  # distinct seeded rows per rank
         theta = W.thetas(B, circ.n_params, 1000 + rank) if args.config != 2 else \
             W.qaoa_thetas(B, 5, 1000 + rank)
     C = tcx.Circuit(circ, dtype, tile_bits=args.tile_bits, coalesce_bits=args.coalesce_bits,

@@ -361,4 +361,12 @@ def config(idx: int, B: Optional[int] = None, n: Optional[int] = None):
         H = tfim_zz_x(n)
         th = thetas(B or 1, c.n_params, 5)
         return "cfg5_hea33_d4_tfim_c64", c, H, th, "c64"
+    if idx == 5:  # not a BASELINE config: the paper's Table VII task
+        n = n or 10
+        c = barren_plateau(n, 10)
+        H = pauli_sum(n, [({0: "Z", 1: "Z"}, 1.0)])
+        rng = np.random.default_rng(6)
+        Bn = B or 100
+        th = np.concatenate([rng.uniform(0, 2 * np.pi, (Bn, n * 10)), rng.uniform(0, 1, (Bn, n * 10))], 1)
+        return "table7_bp10_l10_c64", c, H, th, "c64"
     raise ValueError(idx)
