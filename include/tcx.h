@@ -114,7 +114,9 @@ typedef struct {
                                each as one 2^k x 2^k complex contraction over the state
                                (north_star step 2); 0 = window passes only.
                                Not with global_bits; grad needs k <= 4. */
-    int32_t reserved;
+    int32_t q_grad;         /* 1: window plans also accumulate the real parts of the R' Pauli
+                               components, so tcx_grad_batch_q works on them (per-circuit
+                               kernels only); 0 = off (dense plans always support it) */
 } tcx_build_opts;
 
 /* Executed-plan summary (for reports and tests). */
@@ -206,9 +208,10 @@ tcx_status tcx_state_batch_in(const tcx_circuit* circ, const double* theta, int6
 
 /* <psi|H|d psi/d theta>: its real part is grad / 2, its
  * imaginary part is written to q_im[b][p] (device [B][n_params] float64); E and grad as in
- * tcx_grad_batch.  Produced by the dense-block adjoint (which keeps the full 2^k x 2^k
- * R' = sum psi lambda^dagger): the circuit must be built with dense_k in 1..4, else
- * TCX_E_UNSUPPORTED.  ws sized with TCX_WS_GRAD. */
+ * tcx_grad_batch.  Needs the real parts of R' = sum psi lambda^dagger: dense plans
+ * (dense_k in 1..4, full 2^k x 2^k R') or window plans built with q_grad = 1 (three more
+ * Pauli components per fused op, per-circuit kernels); else TCX_E_UNSUPPORTED.  ws sized
+ * with TCX_WS_GRAD. */
 tcx_status tcx_grad_batch_q(const tcx_circuit* circ, const tcx_pauli* pauli,
                             const double* theta, int64_t B, double* E, double* grad,
                             double* q_im, void* ws, size_t ws_bytes, void* cuda_stream);

@@ -238,9 +238,13 @@ int op_mats(const Op& o) {
     default: return 2 * ((int)o.terms.size() + (o.lut ? 1 : 0));
   }
 }
+thread_local bool g_q_grad = false;  // set per build_plan (this thread's plan)
 int op_accs(const Op& o) {
   if (!o.has_param) return 0;
-  return o.type == OP_U1 ? 3 : o.nslots;  // U1: Pauli components (cX, cY, cZ) of R
+  // U1: Pauli components (cX, cY, cZ) of R' (Im parts), + (rX, rY, rZ) real parts with
+  // q_grad; DIAG: one Im(lambda* psi) sum per slot, + one Re sum per slot
+  const int base = o.type == OP_U1 ? 3 : o.nslots;
+  return g_q_grad ? 2 * base : base;
 }
 
 struct Budget {
@@ -868,6 +872,7 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
   P.h = t - r;
   P.max_ops_per_pass = opts ? std::max(0, opts->max_ops_per_pass) : 0;
   P.dense_k = opts ? opts->dense_k : 0;
+  P.q_grad = opts && opts->q_grad != 0 && gb == 0;
   if (P.dense_k < 0 || P.dense_k > kMaxDenseK) {
     err = "dense_k must be in [0, 5]";
     return TCX_E_INVALID;
@@ -1010,6 +1015,7 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
 
   // ---- pass scheduling
   g_packed_u1 = dtype == TCX_C64;
+  g_q_grad = P.q_grad && P.dense_k == 0;
   Scheduler S(P);
   S.lookahead = gb == 0 && P.ops.size() <= 4096 && !(getenv("TCX_PLAN_GREEDY"));
   const int rb = c128 ? 8 : 4;  // bytes per Real
@@ -1313,6 +1319,7 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
         GItem gi{};
         gi.type = OP_U1;
         gi.acc = o.acc_off;
+        gi.re_acc = g_q_grad ? o.acc_off + 3 : -1;
         gi.cons_begin = mi.cons_begin;
         gi.cons_count = mi.cons_count;
         gi.contrib = -1;
@@ -1358,6 +1365,7 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
         GItem gi{};
         gi.type = OP_DIAG;
         gi.acc = o.acc_off + tm.slot;
+        gi.re_acc = g_q_grad ? o.acc_off + o.nslots + tm.slot : -1;
         gi.factor = -2.0 * tm.w;
         gi.contrib = contrib++;
         contrib_param.push_back(tm.param);

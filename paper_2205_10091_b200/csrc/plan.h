@@ -81,10 +81,11 @@ struct DCons {       // device copy of Constituent
 };
 struct GItem {       // finalize items
   int32_t type;      // OP_U1: R' -> constituent contributions; OP_DIAG: scalar slot
-  int32_t acc;       // global slot (U1: 8 slots)
+  int32_t acc;       // global slot (U1: 3 Im components, + 3 Re components with q_grad)
   int32_t cons_begin, cons_count;
   double factor;     // DIAG: -2 * w
-  int32_t contrib, pad;
+  int32_t contrib;
+  int32_t re_acc;    // q_grad: slot of the real-part sums (U1: acc + 3), else -1
 };
 
 // Dense k-qubit block (north_star step 2): a run of gates fused into one
@@ -192,6 +193,7 @@ struct Plan {
   uint64_t fold_mask = 0;          // bits whose leading U1 op is folded into the initial state
   double init_amp = 1.0;           // 2^(-popc(init_hmask)/2)
   int dense_k = 0;                 // > 0: gates run as dense k-qubit blocks (tcx_build_opts)
+  bool q_grad = false;             // window plan also accumulates Re R' components
   std::vector<DBlock> dblocks;     // in execution order (before the window passes)
   std::vector<DGate> dgates;
   int dmat_row = 0;                // complex entries per theta row (parameterised blocks)

@@ -181,6 +181,7 @@ struct FinArgs {
   int ncontrib;
   double* tot;          // [B][K]
   double* contrib;      // [B][ncontrib]
+  double* qcontrib;     // optional [B][ncontrib]: Im <psi|H|d psi> contributions (q_grad)
   double* E;
   double* grad;         // may be null
   int64_t b0;
@@ -222,7 +223,9 @@ __global__ void finalize_kernel(const FinArgs a) {
   for (int gi = tid; gi < a.ngitems; gi += nt) {
     const GItem g = a.gitems[gi];
     if (g.type == OP_DIAG) {
-      ctb[g.contrib] = g.factor * tot[g.acc];
+      ctb[g.contrib] = g.factor * tot[g.acc];  // 2 Re q
+      if (a.qcontrib && g.re_acc >= 0)           // Im q = w sum s Re(lambda* psi)
+        a.qcontrib[b * a.ncontrib + g.contrib] = -0.5 * g.factor * tot[g.re_acc];
       continue;
     }
     // Pauli components of R' (device_common.cuh accum_c3): Im Tr(B R') = bx c0 + by c1 + bz c2
@@ -242,6 +245,9 @@ __global__ void finalize_kernel(const FinArgs a) {
         // B Hermitian traceless: B = bx X + by Y + bz Z, B01 = bx - i by, B00 = bz
         const double bx = Bm[1].x, by = -Bm[1].y, bz = Bm[0].x;
         ctb[cn.contrib] = cn.coeff * (bx * c3[0] + by * c3[1] + bz * c3[2]);
+        if (a.qcontrib && g.re_acc >= 0)  // Im q = -coeff Re Tr(B R') / 2
+          a.qcontrib[b * a.ncontrib + cn.contrib] =
+              -0.5 * cn.coeff * (bx * tot[g.re_acc] + by * tot[g.re_acc + 1] + bz * tot[g.re_acc + 2]);
       }
       cdd G[4];
       gate1(cn, th, a.fixed, G);
@@ -588,6 +594,8 @@ WsLayout ws_layout(const Plan& P, const Binding* Bd, int64_t B, int kind, bool h
       w.dq = take((size_t)B * std::max(P.n_contrib, 1) * 8);
     }
   }
+  if (P.dblocks.empty() && P.q_grad && kind == K_GRAD)
+    w.dq = take((size_t)B * std::max(P.n_contrib, 1) * 8);
   if (host_io) {
     w.theta = take(B * std::max(P.P, 1) * 8);
     w.E = take(B * 8);
@@ -1177,11 +1185,18 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
       f.ncontrib = std::max(P.n_contrib, 1);
       f.tot = (double*)(W + wl.tot);
       f.contrib = (double*)(W + wl.contrib);
+      f.qcontrib = (qim && !dense) ? (double*)(W + wl.dq) : nullptr;
       f.E = E;
       f.grad = kind == K_GRAD && P.P > 0 ? grad : nullptr;
       f.b0 = b0;
       finalize_kernel<<<(unsigned)rows, 256, 0, st>>>(f);
       CUDA_TRY(cudaGetLastError());
+      if (f.qcontrib && P.P > 0) {  // window q_grad plans: per-parameter CSR sums
+        dense_qim_kernel<<<dim3((P.P + 127) / 128, (unsigned)rows), 128, 0, st>>>(
+            f.qcontrib, f.ncontrib, (const int32_t*)DT->pptr.p, (const int32_t*)DT->plist.p, P.P,
+            qim, b0);
+        CUDA_TRY(cudaGetLastError());
+      }
     }
   } else if (!one && !keep_state) {
     const size_t bytes = (size_t)B * ((size_t)1 << P.n) * 2 * rs;
@@ -1324,9 +1339,10 @@ tcx_status tcx_grad_batch_q(const tcx_circuit* circ, const tcx_pauli* pauli, con
   g_err.clear();
   if (!circ || !q_im) return fail(TCX_E_INVALID, "null circuit or q_im");
   Plan& P = const_cast<tcx_circuit*>(circ)->plan;
-  if (P.dblocks.empty())
+  if (P.dblocks.empty() && !(P.q_grad && P.jit_on))
     return fail(TCX_E_UNSUPPORTED,
-                "Im <psi|H|d psi> is produced by the dense-block adjoint: build with dense_k in 1..4");
+                "Im <psi|H|d psi> needs a dense plan (dense_k in 1..4) or a window plan built "
+                "with q_grad = 1 (per-circuit kernels)");
   return run(P, pauli, theta, B, E, grad, nullptr, ws, ws_bytes, (cudaStream_t)stream, K_GRAD,
              nullptr, nullptr, nullptr, false, q_im);
 }

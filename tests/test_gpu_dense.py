@@ -174,3 +174,34 @@ def test_psi_h_dpsi_dense(tc, dtype, k):
     check_E(E.cpu().numpy(), np.array([r[0] for r in ref]), H, dtype)
     check_grad(G.cpu().numpy(), np.array([r[1] for r in ref]), H, c, dtype)
     check_grad(2 * Q.cpu().numpy(), 2 * np.array([r[2] for r in ref]), H, c, dtype, "q_im")
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("opts", [{}, {"tile_bits": 7, "coalesce_bits": 2}])
+@pytest.mark.parametrize("seed", [1, 2])
+def test_psi_h_dpsi_window_q_grad(tc, dtype, opts, seed):
+    """Window plans built with q_grad = 1 accumulate the real parts of the R' Pauli
+    components (general and structured U1 classes) and of the diagonal-term sums (grouped and
+    LUT phases): Im <psi|H|d psi/d theta> vs the oracle."""
+    n = 10
+    c = W.random_circuit(n, 80, 7300 + seed, n_params=6, with_payload=True)
+    H = W.random_pauli_sum(n, 9, 73 + seed)
+    th = W.thetas(3, 6, seed)
+    C, P = tc.Circuit(c, dtype, q_grad=True, **opts), tc.Pauli(H)
+    E, G, Q = tc.grad_batch_q(C, P, _th(th))
+    ref = [orc.value_qgrad(c, H, th[b]) for b in range(3)]
+    check_E(E.cpu().numpy(), np.array([r[0] for r in ref]), H, dtype)
+    check_grad(G.cpu().numpy(), np.array([r[1] for r in ref]), H, c, dtype)
+    check_grad(2 * Q.cpu().numpy(), 2 * np.array([r[2] for r in ref]), H, c, dtype, "q_im")
+    # the same plan's plain gradient is unchanged
+    E2, G2 = tc.grad_batch(C, P, _th(th))
+    assert np.array_equal(G2.cpu().numpy(), G.cpu().numpy())
+
+
+def test_psi_h_dpsi_window_qaoa_lut(tc):
+    """QAOA (LUT diagonal cost layers, XT mixers, H folded into the init) with q_grad."""
+    name, c, H, th, dt = W.config(2, B=2, n=10)
+    C, P = tc.Circuit(c, "c128", q_grad=True), tc.Pauli(H)
+    E, G, Q = tc.grad_batch_q(C, P, _th(th))
+    ref = [orc.value_qgrad(c, H, th[b]) for b in range(2)]
+    check_grad(2 * Q.cpu().numpy(), 2 * np.array([r[2] for r in ref]), H, c, "c128", "q_im")
