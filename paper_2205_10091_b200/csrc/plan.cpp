@@ -890,7 +890,6 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
   // two lock-stepped sub-tiles (512 threads) share one instruction stream in the JIT
   // kernels when tiles pair up and a sub-tile has whole warps
   P.jit_nsub = 1;  // 2 = lock-stepped sub-tiles (measured slower with FFMA2 code; opt-in via TCX_JIT_NSUB)
-  if (const char* e = getenv("TCX_JIT_DBUF")) P.jit_dbuf = atoi(e) != 0;
   if (const char* e = getenv("TCX_JIT_NSUB"))
     if (atoi(e) == 2 && P.tpc % 2 == 0 && P.h >= 5) P.jit_nsub = 2;
   // ---- lower

@@ -188,8 +188,6 @@ struct Plan {
   int64_t tiles = 1;             // 2^(n - t)
   int tpc = 1;                   // tiles per CTA (depends on the tile count only, never on B)
   int jit_nsub = 1;              // lock-stepped sub-tiles per CTA in JIT kernels
-  bool jit_dbuf = false;         // forward JIT kernels: two exchange buffers, one barrier per
-                                 // register-stage transition (the lambda buffer is reused)
 
   uint64_t init_hmask = 0;         // leading H gates folded into the initial state (bits)
   uint64_t fold_mask = 0;          // bits whose leading U1 op is folded into the initial state

@@ -941,10 +941,8 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
             a.use_tma = (wl.lam == 0 || encode_tmap(a.tmap[1], a.lam, td, P.nloc, B)) ? 1 : 0;
           if (!(a.mode & (M_LOAD_PSI | M_LOAD_LAM | M_STORE_PSI | M_STORE_LAM))) a.use_tma = 0;
         }
-        // forward JIT kernels with double-buffered transitions also use the lambda buffer
-        const bool two_j = two || (fwd && !two && P.jit_dbuf && ns == 1 && jkey[0] == 'p');
         const SmemLayout LJ = smem_layout(a.t, a.h, rs, a.mat_count, a.max_stage_acc,
-                                          (a.mode & M_BWD) ? a.acc_count : 0, a.nstages, two_j, ns);
+                                          (a.mode & M_BWD) ? a.acc_count : 0, a.nstages, two, ns);
         if (LJ.total > 227 * 1024 - 1280)
           return fail(TCX_E_UNSUPPORTED, "JIT pass needs too much shared memory");
         if (LJ.total > 48 * 1024 && (size_t)LJ.total > DT->jit_smem[jkey]) {
