@@ -234,7 +234,9 @@ def main():
     # CUDA graph of one step (streams and graphs instead of a tracing compiler): the
     # library's launches are plain stream work once its JIT modules and tables exist
     graph, graph_note = None, "eager"
-    if args.graph:
+    # single-process only: a captured NCCL collective that fails to instantiate could leave
+    # the communicator unusable mid-run, and multi-GPU steps are not launch-bound
+    if args.graph and world == 1:
         try:
             gs = torch.cuda.Stream(dev)
             gs.wait_stream(stream)
