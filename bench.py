@@ -164,9 +164,10 @@ def main():
     ap.add_argument("--jit", type=int, default=1, help="1: per-circuit specialised kernels")
     ap.add_argument("--mode", default=None, choices=["grad", "expect"],
                     help="grad (E + adjoint gradient, default) or expect (forward + E only; cfg4)")
-    ap.add_argument("--graph", type=int, default=1,
+    ap.add_argument("--graph", type=int, default=-1,
                     help="1: capture one step (library kernels + all-reduce) in a CUDA graph and "
-                         "replay it (launch-bound small configs); 0: eager launches")
+                         "replay it; 0: eager launches; -1 (default): graph only for launch-bound "
+                         "steps (< 2 ms eager), so long steps keep per-kernel events in the timed region")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-rows", type=int, default=8)
     ap.add_argument("--virtual-ranks", type=int, default=1,
@@ -228,15 +229,20 @@ def main():
             Ex = tcx.expect_batch(C, P, th, stream=stream, ws=ws)
             allreduce_loss_grad(Ex, G[:, :0], out=red[:1])
 
-    for _ in range(args.warmup):
+    w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for i in range(args.warmup):
+        if i == args.warmup - 1:
+            w0.record(stream)
         step()
+    w1.record(stream)
     torch.cuda.synchronize(dev)
+    use_graph = args.graph == 1 or (args.graph == -1 and w0.elapsed_time(w1) < 2.0)
     # CUDA graph of one step (streams and graphs instead of a tracing compiler): the
     # library's launches are plain stream work once its JIT modules and tables exist
     graph, graph_note = None, "eager"
     # single-process only: a captured NCCL collective that fails to instantiate could leave
     # the communicator unusable mid-run, and multi-GPU steps are not launch-bound
-    if args.graph and world == 1:
+    if use_graph and world == 1:
         try:
             gs = torch.cuda.Stream(dev)
             gs.wait_stream(stream)
@@ -259,6 +265,8 @@ def main():
     clocks.start()
     time.sleep(0.3)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if graph is None:  # per-kernel CUDA events live inside the timed region
+        tcx.profile_enable(True)
     e0.record(stream)
     for _ in range(args.steps):
         if graph is not None:
@@ -268,13 +276,14 @@ def main():
     e1.record(stream)
     torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1)
-    # per-kernel device times for the roofline: one extra eager, profiled step
-    tcx.profile_enable(True)
-    step()
-    torch.cuda.synchronize(dev)
+    prof_steps = args.steps
+    if graph is not None:  # graph replays carry no per-kernel events: one extra eager step
+        tcx.profile_enable(True)
+        step()
+        torch.cuda.synchronize(dev)
+        prof_steps = 1
     tcx.profile_enable(False)
     prof = tcx.profile_read()
-    prof_steps = 1
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
@@ -384,7 +393,9 @@ def main():
                                                  "n_ops", "jit", "dense_k", "dense_blocks")},
                    "jit_compile_s": round(t_jit, 2), "mode": mode,
                    "max_ops_per_pass": args.max_ops_per_pass, "dense_k": args.dense_k,
-                   "launch": graph_note + "; per-kernel times from one extra eager profiled step"},
+                   "launch": graph_note + ("; per-kernel times from one extra eager profiled step"
+                                           if graph is not None else
+                                           "; per-kernel CUDA events inside the timed region")},
         "roofline": roof,
         "kernels": kernel_split,
         "cpu_baseline": cpu,
