@@ -369,3 +369,36 @@ def test_batch_above_grid_y_limit(tc, opts):
     check_grad(G.cpu().numpy()[rows], Gr, H, c, "c128")
     Et = tc.expect_terms_batch(C, P, _th(th)).cpu().numpy()
     assert np.abs((Et * H.weights).sum(1) - E.cpu().numpy()).max() <= 1e-11 * H.l1
+
+
+# ------------------------------------------------------------ full-size cfg4
+@pytest.mark.slow
+def test_cfg4_full_circuit_norm():
+    """configs[3] at full size in the bench configuration (n = 30, 200 layers, complex128,
+    light-cone window passes): <I> = |psi|^2 = 1 (unitarity) and |<Z_0>| <= 1."""
+    import torch
+    from paper_2205_10091_b200 import tcx
+    name, c, H, th, dt = W.config(3)
+    C = tcx.Circuit(c, dt)
+    Hs = W.pauli_sum(c.n, [({}, 1.0), ({0: "Z"}, 1.0)])
+    Et = tcx.expect_terms_batch(C, tcx.Pauli(Hs), _th(th)).cpu().numpy()[0]
+    assert abs(Et[0] - 1.0) < 1e-10 and abs(Et[1]) <= 1.0 + 1e-10
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.slow
+def test_cfg4_window_roundtrip_30q():
+    """n = 30 complex128 through the window passes (the bench's path): 20 random layers then
+    their inverse return |0...0> (sampled amplitudes)."""
+    import torch
+    from paper_2205_10091_b200 import tcx
+    c = W.random_deep_circuit(30, 20, 4)
+    full = W.Circuit(30, 0)
+    full.gates = list(c.gates) + [W.Gate(g.name, g.q0, g.q1, -1, -g.coeff if g.name in ("rx", "ry", "rz") else g.coeff)
+                                  for g in reversed(c.gates)]
+    psi = tcx.state_batch(tcx.Circuit(full, "c128"), _th(np.zeros((1, 0))))
+    assert abs(complex(psi[0, 0].item()) - 1.0) < 1e-11
+    idx = torch.randint(1, 1 << 30, (4096,), generator=torch.Generator().manual_seed(1)).cuda()
+    assert psi[0, idx].abs().max().item() < 1e-11
+    del psi
+    torch.cuda.empty_cache()
