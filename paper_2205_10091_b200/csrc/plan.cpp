@@ -769,6 +769,15 @@ void build_dense(Plan& P, const tcx_gate* gates, int64_t G, int* pos,
   }
   std::sort(open.begin(), open.end(), [](const Open& a, const Open& b) { return a.order < b.order; });
   for (auto& o : open) emit(o);
+  // adjoint shortcut (as for window ops): later-processed blocks read only partial traces
+  // over their complement, invariant under a unitary on bits no earlier block touches
+  uint64_t touched = 0;
+  for (auto& d : P.dblocks) {
+    uint64_t m = 0;
+    for (int i = 0; i < d.k; ++i) m |= 1ull << d.bits[i];
+    d.first = (m & touched) == 0 ? 1 : 0;
+    touched |= m;
+  }
 }
 
 tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const double* mats,

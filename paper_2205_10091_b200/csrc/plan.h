@@ -106,6 +106,8 @@ struct DBlock {
   int32_t mat_off;            // complex offset of U (row-major 2^k x 2^k) in its table
   int32_t acc_off;            // backward: offset of the block's Q partials (2^(2k) reals)
   int32_t has_param;
+  int32_t first;              // 1: no earlier block touches these bits -> the backward needs
+                              // only R' here, not U^dagger on psi / lambda (plan.cpp)
 };
 
 struct PassInfo {

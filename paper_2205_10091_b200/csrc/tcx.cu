@@ -1097,7 +1097,7 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
       const int Sd = dense_bwd_ctas(P);
       for (int di = (int)P.dblocks.size() - 1; di >= 0; --di) {
         const DBlock& blk = P.dblocks[di];
-        if (di == 0 && !blk.has_param) continue;  // nothing left to compute
+        if ((di == 0 || blk.first) && !blk.has_param) continue;  // nothing left to compute
         ProfEntry pe{};
         if (g_prof.on) {
           CUDA_TRY(cudaEventCreate(&pe.a));
@@ -1108,7 +1108,7 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
           const int64_t rows = std::min(kMaxRows, B - b0);
           DenseArgs d;
           dense_args(d, blk);
-          d.store = di > 0 ? 1 : 0;
+          d.store = (di > 0 && !blk.first) ? 1 : 0;
           d.part = blk.has_param ? (double*)(W + wl.dpart) : nullptr;
           d.b0 = b0;
           cudaError_t e = c128 ? dense_bwd<double>(blk.k, d, Sd, rows, st)
@@ -1126,8 +1126,9 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
           CUDA_TRY(cudaEventRecord(pe.b, st));
           pe.phase = 7;
           pe.index = di;
-          pe.flops = Bf * Nf * 8.0 * (double)(1 << blk.k) * (blk.has_param ? 3.0 : 2.0);
-          pe.bytes = Bf * Nf * csz * (di > 0 ? 4.0 : 2.0);
+          const bool st_ = di > 0 && !blk.first;  // U^dagger applied and stored
+          pe.flops = Bf * Nf * 8.0 * (double)(1 << blk.k) * ((blk.has_param ? 1.0 : 0.0) + (st_ ? 2.0 : 0.0));
+          pe.bytes = Bf * Nf * csz * (st_ ? 4.0 : 2.0);
           g_prof.log.push_back(pe);
         }
       }
