@@ -436,6 +436,7 @@ struct StageOut {
 
 // Stage scheduling inside one pass: ops run in the stage whose register set covers
 // their non-diagonal bits (relaxed locality for CX controls and diagonals).
+static const double g_cx_bonus = getenv("TCX_CX_BONUS") ? atof(getenv("TCX_CX_BONUS")) : 1.0;
 void schedule_stages(Plan& P, const PassInfo& pass, std::vector<StageOut>& stages) {
   const int t = P.t, r = P.r, h = P.h;
   std::vector<int> loc(P.n, -1);
@@ -464,6 +465,9 @@ void schedule_stages(Plan& P, const PassInfo& pass, std::vector<StageOut>& stage
       if (ok) {
         accs += op_accs(o);
         s += op_weight(o);
+        // a CNOT whose control is also a register slot is a free rename; with an outside
+        // control it becomes predicated register swaps (TCX_CX_BONUS tunes the preference)
+        if (o.type == OP_CX && loc[o.b1] >= 0 && (R >> loc[o.b1] & 1)) s += g_cx_bonus;
         if (out) out->push_back((int)i);
       } else {
         blocked |= o.bits;
