@@ -1222,7 +1222,7 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
 extern "C" {
 
 const char* tcx_last_error(void) { return g_err.c_str(); }
-const char* tcx_version(void) { return "tcx 0.1 (sm_100a)"; }
+const char* tcx_version(void) { return "tcx 0.2 (sm_100a)"; }
 
 tcx_status tcx_circuit_build(int32_t n_qubits, int32_t n_params, const tcx_gate* gates,
                              int64_t n_gates, const double* matrices, int64_t n_matrix_elems,
