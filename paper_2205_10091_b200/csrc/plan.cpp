@@ -900,10 +900,6 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
   }
   P.tiles = 1ll << (n - gb - t);
   P.tpc = (int)std::min<int64_t>(64, std::max<int64_t>(1, P.tiles / 32));
-  if (const char* e = getenv("TCX_TPC")) {  // experiments: tiles per CTA (power of two)
-    const int v = atoi(e);
-    if (v > 0 && P.tiles % v == 0) P.tpc = v;
-  }
   // two lock-stepped sub-tiles (512 threads) share one instruction stream in the JIT
   // kernels when tiles pair up and a sub-tile has whole warps
   P.jit_nsub = 1;  // 2 = lock-stepped sub-tiles (measured slower with FFMA2 code; opt-in via TCX_JIT_NSUB)
