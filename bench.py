@@ -157,6 +157,8 @@ def main():
     ap.add_argument("--coalesce-bits", type=int, default=0)
     ap.add_argument("--reg-bits", type=int, default=0)
     ap.add_argument("--max-ops-per-pass", type=int, default=0)
+    ap.add_argument("--l2-rows", type=int, default=0,
+                    help="theta rows per L2-resident group (-1 auto; 0 off)")
     ap.add_argument("--dtype", default=None, choices=["c64", "c128"],
                     help="override the config's state dtype (studies; e.g. cfg4 at complex64)")
     ap.add_argument("--dense-k", type=int, default=0,
@@ -205,7 +207,7 @@ def main():
     C = tcx.Circuit(circ, dtype, tile_bits=args.tile_bits, coalesce_bits=args.coalesce_bits,
                     reg_bits=args.reg_bits,
                     max_ops_per_pass=args.max_ops_per_pass,
-                    jit=bool(args.jit), dense_k=args.dense_k)
+                    jit=bool(args.jit), dense_k=args.dense_k, l2_rows=args.l2_rows)
     P = tcx.Pauli(H)
     t_jit = time.perf_counter()
     mode = args.mode or ("expect" if circ.n_params == 0 else "grad")
@@ -393,6 +395,7 @@ def main():
                                                  "n_ops", "jit", "dense_k", "dense_blocks")},
                    "jit_compile_s": round(t_jit, 2), "mode": mode,
                    "max_ops_per_pass": args.max_ops_per_pass, "dense_k": args.dense_k,
+                   "l2_rows": args.l2_rows,
                    "launch": graph_note + ("; per-kernel times from one extra eager profiled step"
                                            if graph is not None else
                                            "; per-kernel CUDA events inside the timed region")},

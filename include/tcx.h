@@ -117,6 +117,10 @@ typedef struct {
     int32_t q_grad;         /* 1: window plans also accumulate the real parts of the R' Pauli
                                components, so tcx_grad_batch_q works on them (per-circuit
                                kernels only); 0 = off (dense plans always support it) */
+    int32_t l2_rows;        /* L2-resident row groups: > 0 runs all passes for
+                               groups of this many theta rows in turn, so a group's psi and
+                               lambda stay in L2 between passes; -1 = auto (groups whose psi +
+                               lambda fit ~96 MB); 0 = off (every pass over all rows) */
 } tcx_build_opts;
 
 /* Executed-plan summary (for reports and tests). */

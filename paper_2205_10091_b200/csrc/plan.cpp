@@ -886,6 +886,12 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
   P.max_ops_per_pass = opts ? std::max(0, opts->max_ops_per_pass) : 0;
   P.dense_k = opts ? opts->dense_k : 0;
   P.q_grad = opts && opts->q_grad != 0 && gb == 0;
+  if (opts && opts->l2_rows > 0) {
+    P.l2_rows = opts->l2_rows;
+  } else if (opts && opts->l2_rows < 0) {  // psi + lambda of a group within ~96 MB of L2
+    const double row = 2.0 * (double)((int64_t)1 << (n - gb)) * (dtype == TCX_C128 ? 16.0 : 8.0);
+    P.l2_rows = std::max<int64_t>(1, (int64_t)(96.0e6 / row));
+  }
   if (P.dense_k < 0 || P.dense_k > kMaxDenseK) {
     err = "dense_k must be in [0, 5]";
     return TCX_E_INVALID;

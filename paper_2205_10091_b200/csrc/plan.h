@@ -196,6 +196,7 @@ struct Plan {
   double init_amp = 1.0;           // 2^(-popc(init_hmask)/2)
   int dense_k = 0;                 // > 0: gates run as dense k-qubit blocks (tcx_build_opts)
   bool q_grad = false;             // window plan also accumulates Re R' components
+  int64_t l2_rows = 0;             // > 0: theta rows per L2-resident group (run())
   std::vector<DBlock> dblocks;     // in execution order (before the window passes)
   std::vector<DGate> dgates;
   int dmat_row = 0;                // complex entries per theta row (parameterised blocks)

@@ -787,6 +787,7 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
   const int64_t S = P.tiles / tiles_per_cta(P);
   const int EU = Bd ? (int)Bd->units.size() : 1;
   const int64_t kMaxRows = 65535;
+  int64_t rlo = 0, rhi = B;  // rows of the current L2 row group (all rows unless grouped)
   // ---- materialize per-theta matrices
   for (int64_t b0 = 0; b0 < B && want(0, 0); b0 += kMaxRows) {
     const int64_t rows = std::min(kMaxRows, B - b0);
@@ -928,13 +929,13 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
       tcx_status js = jit_function(P, DT, jkey, &jf);
       if (js) return js;
     }
-    for (int64_t b0 = 0; b0 < B; b0 += kMaxRows) {
-      const int64_t rows = std::min(kMaxRows, B - b0);
+    for (int64_t b0 = rlo; b0 < rhi; b0 += kMaxRows) {
+      const int64_t rows = std::min(kMaxRows, rhi - b0);
       a.b0 = b0;
       if (jf) {
         Drv& D = drv();
         const int ns = jkey[0] == 'p' ? P.jit_nsub : 1;  // lambda kernels: one tile per CTA
-        if (b0 == 0) {
+        if (b0 == rlo) {
           const TmaDims td = tma_dims(P.nloc, a.wmask, c128);
           a.use_tma = 0;
           if (td.rank > 0 && ns == 1 && encode_tmap(a.tmap[0], a.psi, td, P.nloc, B))
@@ -970,7 +971,8 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
     }
     return TCX_OK;
   };
-  const double Nf = (double)((int64_t)1 << P.nloc), csz = 2.0 * rs, Bf = (double)B;
+  const double Nf = (double)((int64_t)1 << P.nloc), csz = 2.0 * rs;
+  double Bf = (double)B;  // rows of the current group (profiling cost model)
   auto launch = [&](PassArgs& a, int phase, int index, double flops_amp) -> tcx_status {
     std::string jkey;
     if (P.jit_on) {
@@ -1015,6 +1017,13 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
                       (kind == K_GRAD ? pass_flops(P, p, true) : 0.0);
     if ((s = launch(a, 5, 0, fl))) return s;
   } else {
+   // L2-resident row groups: all passes of a group of theta rows run before
+   // the next group, so a group's psi and lambda stay in the 126 MB L2 between passes
+   const int64_t G = (P.l2_rows > 0 && P.gbits == 0 && !one) ? std::min<int64_t>(P.l2_rows, B) : B;
+   for (int64_t g0 = 0; g0 < B; g0 += G) {
+    rlo = g0;
+    rhi = std::min(B, g0 + G);
+    Bf = (double)(rhi - rlo);
     const bool sharded = P.gbits > 0;
     for (size_t di = 0; di < P.dblocks.size(); ++di) {
       const DBlock& blk = P.dblocks[di];
@@ -1024,8 +1033,8 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
         CUDA_TRY(cudaEventCreate(&pe.b));
         CUDA_TRY(cudaEventRecord(pe.a, st));
       }
-      for (int64_t b0 = 0; b0 < B; b0 += kMaxRows) {
-        const int64_t rows = std::min(kMaxRows, B - b0);
+      for (int64_t b0 = rlo; b0 < rhi; b0 += kMaxRows) {
+        const int64_t rows = std::min(kMaxRows, rhi - b0);
         DenseArgs d;
         dense_args(d, blk);
         d.init = (di == 0 && !psi0) ? 1 : 0;
@@ -1104,8 +1113,8 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
           CUDA_TRY(cudaEventCreate(&pe.b));
           CUDA_TRY(cudaEventRecord(pe.a, st));
         }
-        for (int64_t b0 = 0; b0 < B; b0 += kMaxRows) {
-          const int64_t rows = std::min(kMaxRows, B - b0);
+        for (int64_t b0 = rlo; b0 < rhi; b0 += kMaxRows) {
+          const int64_t rows = std::min(kMaxRows, rhi - b0);
           DenseArgs d;
           dense_args(d, blk);
           d.store = (di > 0 && !blk.first) ? 1 : 0;
@@ -1133,6 +1142,10 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
         }
       }
     }
+   }  // row groups
+   rlo = 0;
+   rhi = B;
+   Bf = (double)B;
   }
   // ---- dense block gradient contributions (before finalize sums them per parameter)
   if (kind == K_GRAD && dense && P.dacc_total > 0 && want(4, 0)) {

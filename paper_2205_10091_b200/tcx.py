@@ -45,7 +45,8 @@ class tcx_build_opts(ctypes.Structure):
     _fields_ = [("tile_bits", ctypes.c_int32), ("reg_bits", ctypes.c_int32),
                 ("coalesce_bits", ctypes.c_int32), ("max_ops_per_pass", ctypes.c_int32),
                 ("jit", ctypes.c_int32), ("global_bits", ctypes.c_int32),
-                ("dense_k", ctypes.c_int32), ("q_grad", ctypes.c_int32)]
+                ("dense_k", ctypes.c_int32), ("q_grad", ctypes.c_int32),
+                ("l2_rows", ctypes.c_int32)]
 
 
 class tcx_plan_info(ctypes.Structure):
@@ -150,7 +151,8 @@ class Circuit:
 
     def __init__(self, circ, dtype: str = "c64", tile_bits: int = 0, reg_bits: int = 0,
                  coalesce_bits: int = 0, max_ops_per_pass: int = 0, jit: bool = True,
-                 global_bits: int = 0, gates=None, dense_k: int = 0, q_grad: bool = False):
+                 global_bits: int = 0, gates=None, dense_k: int = 0, q_grad: bool = False,
+                 l2_rows: int = 0):
         names, q0, q1, param, coeff, moff, mats = circ.arrays()
         self.n = circ.n
         self.P = circ.n_params
@@ -162,7 +164,7 @@ class Circuit:
             mats = np.zeros(2)
         self._mats = mats
         opts = tcx_build_opts(tile_bits, reg_bits, coalesce_bits, max_ops_per_pass,
-                              0 if jit else -1, global_bits, dense_k, 1 if q_grad else 0)
+                              0 if jit else -1, global_bits, dense_k, 1 if q_grad else 0, l2_rows)
         self.global_bits = global_bits
         h = _vp()
         _check(_lib.tcx_circuit_build(self.n, self.P, self._gates, self.G,

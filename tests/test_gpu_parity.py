@@ -402,3 +402,18 @@ def test_cfg4_window_roundtrip_30q():
     assert psi[0, idx].abs().max().item() < 1e-11
     del psi
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("opts", [{"tile_bits": 8, "coalesce_bits": 2}, {"dense_k": 2}, {"jit": False}])
+def test_l2_row_groups(tc, opts):
+    """L2-resident row groups: B = 5 rows in groups of 2 give the same E and
+    gradient as one pass over all rows (bitwise: rows are independent and each row's
+    reductions keep their order)."""
+    c, H = W.hea(11, 2), W.heisenberg(11)
+    th = W.thetas(5, c.n_params, 8)
+    E1, G1, _ = run_grad(tc, c, H, th, "c64", **opts)
+    E2, G2, _ = run_grad(tc, c, H, th, "c64", l2_rows=2, **opts)
+    assert np.array_equal(E1, E2) and np.array_equal(G1, G2)
+    Er, Gr = oracle_grad(c, H, th)
+    check_E(E2, Er, H, "c64")
+    check_grad(G2, Gr, H, c, "c64")
