@@ -475,7 +475,15 @@ tcx_status jit_function(Plan& P, DeviceTables* DT, const std::string& key, CUfun
 }
 
 // Compile every specialised kernel a call of this kind needs, in parallel, before launching.
-tcx_status jit_prepare(Plan& P, int kind, bool mega, const Binding* Bd) {
+// grad with one lambda unit: the last forward pass, lambda = H psi and that pass's backward
+// run as one kernel per tile (no store / reload of psi and lambda in between)
+bool fuse_last_of(const Plan& P, int kind, bool mega, const Binding* Bd) {
+  static const bool no_fuse = getenv("TCX_NO_FUSE_LAST") != nullptr;
+  return !no_fuse && kind == 1 && !mega && P.gbits == 0 && P.dblocks.empty() &&
+         P.passes.size() > 1 && Bd && Bd->units.size() == 1;
+}
+
+tcx_status jit_prepare(Plan& P, int kind, bool mega, const Binding* Bd, bool fuse_last) {
   if (!P.jit_on) return TCX_OK;
   std::vector<std::string> keys;
   const int nP = (int)P.passes.size();
@@ -483,6 +491,10 @@ tcx_status jit_prepare(Plan& P, int kind, bool mega, const Binding* Bd) {
     keys.push_back(jit_key_pass(0, kind == 1 ? 2 : 0));
   } else {
     for (int p = 0; p < nP; ++p) {
+      if (fuse_last && p == nP - 1) {  // last pass: forward + lambda + backward in one kernel
+        keys.push_back(jit_key_pass(p, 2));
+        continue;
+      }
       keys.push_back(jit_key_pass(p, 0));
       if (kind == 1) keys.push_back(jit_key_pass(p, 1));
     }
@@ -780,7 +792,8 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
   if (ws_bytes < wl.total)
     return fail(TCX_E_INVALID, "workspace too small: need " + std::to_string(wl.total) +
                                    " bytes, got " + std::to_string(ws_bytes));
-  if ((s = jit_prepare(P, kind, wl.mega, Bd.get()))) return s;
+  const bool fuse_last = !one && fuse_last_of(P, kind, wl.mega, Bd.get());
+  if ((s = jit_prepare(P, kind, wl.mega, Bd.get(), fuse_last))) return s;
   char* W = (char*)ws;
   const bool c128 = P.dtype == TCX_C128;
   const int rs = c128 ? 8 : 4;
@@ -1064,12 +1077,14 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
       if (last && kind != K_STATE) {
         a.mode |= M_LAMBDA | (kind == K_GRAD ? M_STORE_LAM : 0);
         if (kind != K_GRAD && EU == 1) a.mode &= ~M_STORE_PSI;
+        if (fuse_last) a.mode |= M_BWD;  // stores psi_in / lambda_in for pass nP - 2
         a.group_count = Bd->units[0].group_count;
         a.groups = bdv.groups + Bd->units[0].group_begin;
         a.e_index = 0;
       }
       double fl = pass_flops(P, p, false);
       if (last && kind != K_STATE) fl += lambda_flops(*Bd, Bd->units[0]);
+      if (last && fuse_last) fl += pass_flops(P, p, true);
       if ((s = launch(a, 1, pi, fl))) return s;
     }
     if (kind != K_STATE) {
@@ -1094,6 +1109,7 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
     if (kind == K_GRAD) {
       for (int pi = nP - 1; pi >= 0; --pi) {
         if (!want(3, pi)) continue;
+        if (fuse_last && pi == nP - 1) continue;  // ran fused with the last forward pass
         const PassInfo& p = P.passes[pi];
         if (dense && p.ops.empty()) continue;  // the trailing E / lambda pass has no gates
         int mode = M_LOAD_PSI | M_LOAD_LAM | M_BWD | (pi > 0 ? (M_STORE_PSI | M_STORE_LAM) : 0);
@@ -1496,7 +1512,7 @@ tcx_status tcx_circuit_jit(const tcx_circuit* circ, const tcx_pauli* pauli, int6
     if (s) return s;
   }
   WsLayout wl = ws_layout(P, Bd.get(), B, kind, false);
-  return jit_prepare(P, kind, wl.mega, Bd.get());
+  return jit_prepare(P, kind, wl.mega, Bd.get(), fuse_last_of(P, kind, wl.mega, Bd.get()));
 }
 
 tcx_status tcx_circuit_info(const tcx_circuit* circ, const tcx_pauli* pauli, tcx_plan_info* o) {
@@ -1704,7 +1720,8 @@ tcx_status tcx_launch_count(const tcx_circuit* circ, const tcx_pauli* pauli, int
     per += 1;
   else
     per += (int64_t)P.passes.size() + (int64_t)Bd->units.size() - 1 +
-           (want_grad ? (int64_t)P.passes.size() : 0);
+           (want_grad ? (int64_t)P.passes.size() : 0) -
+           (fuse_last_of(P, kind, wl.mega, Bd.get()) ? 1 : 0);
   per += 1;  // finalize
   *launches = (int32_t)(per * chunks);
   return TCX_OK;
