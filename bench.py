@@ -109,14 +109,53 @@ def cpu_oracle_rows(circ, H, theta, threads, mode="grad"):
     return time.perf_counter() - t0
 
 
+def host_cpu():
+    """(logical cores, CPU model) of this host, recorded with every oracle figure."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return os.cpu_count() or 1, model
+
+
+def cpu_baseline(circ, H, theta, mode, name, max_rows=0):
+    """SURVEY §8d oracle timing on this host: (i) one theta row on one thread, (ii) the same
+    oracle with OpenMP over theta rows on every host core (one row per core).  Bounded
+    samples of the workload (whole rows), linear in rows; cfg5's 2^33 state does not fit the
+    oracle (closed-form pinned instead) and cfg4 has B = 1 (row-parallel OpenMP cannot use
+    more than one core there), so those report the single-thread figure only."""
+    nproc, model = host_cpu()
+    if circ.n > 28:
+        return {"value": None, "unit": "circuits/s", "cores": 0, "kind": "oracle",
+                "nproc": nproc, "cpu_model": model,
+                "sample": f"N/A: a {circ.n}-qubit state does not fit the float64 oracle"}
+    t1 = cpu_oracle_rows(circ, H, theta[:1], 1, mode)
+    single = {"value": 1.0 / t1, "cores": 1, "sample": f"1 theta row of {name}, {t1:.1f} s"}
+    rows = min(nproc, theta.shape[0]) if not max_rows else min(nproc, theta.shape[0], max_rows)
+    if rows <= 1:
+        return {"value": single["value"], "unit": "circuits/s", "cores": 1, "kind": "oracle",
+                "nproc": nproc, "cpu_model": model, "sample": single["sample"] +
+                " (B = 1: the oracle parallelises over rows only)", "single_thread": single}
+    tn = cpu_oracle_rows(circ, H, theta[:rows], rows, mode)
+    return {"value": rows / tn, "unit": "circuits/s", "cores": rows, "kind": "oracle",
+            "nproc": nproc, "cpu_model": model,
+            "sample": f"{rows} theta rows of {name}, OpenMP one row per core, {tn:.1f} s",
+            "single_thread": single}
+
+
 def run_reference(args, rank, world):
     """The tier's reference arm: the CPU oracle, as it stands, on host cores."""
     if rank != 0:
         return 0
     name, circ, H, theta, dtype = W.config(args.config, B=args.batch)
     mode = args.mode or ("expect" if circ.n_params == 0 else "grad")
-    cores = os.cpu_count() or 1
-    rows = max(1, min(cores, args.ref_rows))
+    cores, model = host_cpu()
+    rows = max(1, min(cores, args.ref_rows or cores, theta.shape[0]))
     sample = theta[:rows]
     for _ in range(args.warmup):
         cpu_oracle_rows(circ, H, sample[:1], 1, mode)
@@ -134,7 +173,8 @@ def run_reference(args, rank, world):
         "config": {"workload": name, "global_batch": rows, "seq_len": None,
                    "parallelism": "oracle: OpenMP over theta rows"},
         "cpu_baseline": {"value": value, "unit": unit, "cores": rows, "kind": "oracle",
-                         "sample": f"{rows} theta rows of {name} per step (one per core)"},
+                         "nproc": cores, "cpu_model": model,
+                         "sample": f"{rows} theta rows of {name} per step (OpenMP, one per core)"},
         "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -171,10 +211,10 @@ def main():
                          "replay it; 0: eager launches; -1 (default): graph only for launch-bound "
                          "steps (< 2 ms eager), so long steps keep per-kernel events in the timed region")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-rows", type=int, default=8)
+    ap.add_argument("--ref-rows", type=int, default=0, help="reference arm rows (0: one per host core)")
     ap.add_argument("--virtual-ranks", type=int, default=1,
                     help="config 4 on one GPU: shard the state over this many virtual ranks")
-    ap.add_argument("--cpu-rows", type=int, default=8)
+    ap.add_argument("--cpu-rows", type=int, default=0, help="cpu_baseline rows (0: one per host core)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "tcx" else args.warmup
 
@@ -295,7 +335,12 @@ def main():
     ms = float(t.item())
     value = world * B * args.steps / (ms / 1e3)
 
-    # ---- end to end through the host-buffer public API (pinned host memory)
+    # ---- end to end through the host-buffer public API (pinned host memory); the
+    # device-resident run's workspace is released first (cfg5's 128 GiB psi + lambda fits once)
+    used_graph, graph = graph is not None, None
+    ws.clear()
+    torch.cuda.synchronize(dev)
+    torch.cuda.empty_cache()
     th_h = torch.as_tensor(np.ascontiguousarray(theta)).pin_memory()
     E_h = torch.empty(B, dtype=torch.float64).pin_memory()
     G_h = torch.empty(B, max(circ.n_params, 1), dtype=torch.float64).pin_memory()
@@ -353,7 +398,7 @@ def main():
             roof = {"bound": "hbm", "achieved": ach, "peak": hbm_peak / 1e9, "unit": "GB/s",
                     "frac": ach / (hbm_peak / 1e9)}
         jitk = {"forward": "tcx_jit_fwd_*", "backward": "tcx_jit_bwd_*", "lambda": "tcx_jit_lam_*",
-                "fused": "tcx_jit_mega_*"}
+                "fused": "tcx_jit_mega_*", "fused_last": "tcx_jit_mega_* (last pass)"}
         kname = {"dense": "dense_fwd_kernel / dense_fwd_tc_kernel (dense k-qubit blocks)",
                  "dense_backward": "dense_bwd_kernel (dense k-qubit blocks, adjoint)"}.get(
                      dom, (f"{jitk.get(dom, dom)} (per-circuit JIT window passes, {dom})"
@@ -370,11 +415,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cores = os.cpu_count() or 1
-        rows = max(1, min(cores, args.cpu_rows))
-        secs = cpu_oracle_rows(circ, H, theta[:rows], rows, mode)
-        cpu = {"value": rows / secs, "unit": "circuits/s", "cores": rows, "kind": "oracle",
-               "sample": f"{rows} theta rows of {name} (one OpenMP thread per row), {secs:.1f} s"}
+        cpu = cpu_baseline(circ, H, theta, mode, name, args.cpu_rows)
 
     launches = C.launch_count(P, B, mode == "grad") * args.steps
     line = {
@@ -397,7 +438,7 @@ def main():
                    "max_ops_per_pass": args.max_ops_per_pass, "dense_k": args.dense_k,
                    "l2_rows": args.l2_rows,
                    "launch": graph_note + ("; per-kernel times from one extra eager profiled step"
-                                           if graph is not None else
+                                           if used_graph else
                                            "; per-kernel CUDA events inside the timed region")},
         "roofline": roof,
         "kernels": kernel_split,
@@ -417,20 +458,22 @@ def main():
 
 
 def run_sharded(args, world, rank, local, dev):
-    """configs[4]: one (33 + log2 G)-qubit complex64 state sharded over G ranks on its top
-    log2 G qubits (weak scaling), NCCL all-to-all qubit exchanges, TFIM <H> + adjoint grad."""
+    """configs[4]: one complex64 state sharded over G ranks on its top log2 G qubits, TFIM
+    <H> + adjoint grad through tcx_grad_sharded (the library runs every pass, the exchanges
+    and the final sum).  N > 1: 33 + log2 N qubits (weak scaling, 2^33 amplitudes per GPU),
+    library-owned NCCL communicator.  --virtual-ranks G on one GPU: the same program with G
+    in-process ranks at 33 qubits in total (compare with the N = 1 line)."""
     import torch
     import torch.distributed as dist
     from paper_2205_10091_b200 import tcx
-    from paper_2205_10091_b200.shard import ShardedState
+    from paper_2205_10091_b200.shard import ShardedState, exchange_counts
     G = world if world > 1 else args.virtual_ranks
     g = G.bit_length() - 1
     assert 1 << g == G, "G must be a power of two"
-    n = (args.batch_qubits or (33 if world > 1 else 30 - g)) + g
+    n = (args.batch_qubits + g) if args.batch_qubits else (33 + g if world > 1 else 33)
     name, circ, H, theta, dtype = W.config(4, n=n)
-    grp = dist.group.WORLD if world > 1 else None
-    S = ShardedState(circ, H, dtype, g, ranks=[rank] if world > 1 else None, dist_group=grp,
-                     jit=bool(args.jit), device=dev)
+    comm = tcx.Comm.nccl() if world > 1 else tcx.Comm.virtual(G)
+    S = ShardedState(circ, H, dtype, g, comm=comm, jit=bool(args.jit), device=dev)
     t0 = time.perf_counter()
     S.C.compile(S.Pl, B=1, kind="grad")
     t_jit = time.perf_counter() - t0
@@ -443,6 +486,7 @@ def run_sharded(args, world, rank, local, dev):
     torch.cuda.synchronize(dev)
     clocks = ClockSampler(local)
     clocks.start()
+    time.sleep(0.3)
     stream = torch.cuda.current_stream(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     tcx.profile_enable(True)
@@ -458,15 +502,29 @@ def run_sharded(args, world, rank, local, dev):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    kms = sum(p[2] for p in prof)
+    by = {}
+    for ph, idx, kms, fl, byt in prof:
+        d = by.setdefault(ph, [0.0, 0.0, 0.0, 0])
+        d[0] += kms
+        d[1] += fl
+        d[2] += byt
+        d[3] += 1
+    kernel_split = {k: {"ms": v[0] / args.steps, "launches_per_step": v[3] / args.steps,
+                        "tflops": v[1] / max(v[0], 1e-9) / 1e9, "gbs": v[2] / max(v[0], 1e-9) / 1e6}
+                    for k, v in by.items()}
+    xms = by.get("exchange", [0.0])[0] / args.steps
     # e2e: theta from pinned host memory in, E / grad back, every step
     th_h = torch.as_tensor(theta).pin_memory()
+    torch.cuda.synchronize(dev)
     t1 = time.perf_counter()
     for _ in range(args.steps):
         E, Gr = S.run(th_h.to(dev, non_blocking=True))
         E.cpu(), Gr.cpu()
-    e2e_s = time.perf_counter() - t1
+    e2e_s = torch.tensor([time.perf_counter() - t1], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     info = S.C.info(S.Pl)
+    nx1, nx3 = exchange_counts(S.C, S.Pl)
     line = {
         "metric": "sharded single-state <H>+grad circuits/s (%s)" % name,
         "value": args.steps / (ms / 1e3), "unit": "circuits/s", "n_gpus": world,
@@ -474,19 +532,24 @@ def run_sharded(args, world, rank, local, dev):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c64",
         "data": "synthetic",
         "config": {"workload": name, "n_qubits": n, "global_bits": g, "ranks": G,
-                   "virtual_ranks": world == 1, "plan": {k: info[k] for k in (
-                       "fwd_passes", "segments", "lambda_passes", "jit")},
+                   "virtual_ranks": world == 1,
+                   "comm": "NCCL (library-owned communicator)" if world > 1 else
+                           "virtual ranks (in-place swap kernels, one GPU)",
+                   "plan": {k: info[k] for k in ("fwd_passes", "segments", "lambda_passes", "jit")},
+                   "exchanges_per_step": {"psi": nx1, "psi_and_lambda": nx3},
                    "jit_compile_s": round(t_jit, 2),
                    "l2": "inputs larger than L2 (2^%d amplitudes per rank)" % (n - g)},
-        "kernel_ms_per_step": kms / args.steps,
-        "exchange_and_other_ms_per_step": (ms - kms) / args.steps,
-        "e2e": {"value": args.steps / e2e_s, "unit": "circuits/s", "h2d_bytes_per_step": int(theta.size * 8),
-                "d2h_bytes_per_step": int(8 + theta.size * 8)},
+        "kernels": kernel_split,
+        "exchange_ms_per_step": xms,
+        "exchange_share": xms / (ms / args.steps),
+        "e2e": {"value": args.steps / float(e2e_s.item()), "unit": "circuits/s",
+                "h2d_bytes_per_step": int(theta.size * 8), "d2h_bytes_per_step": int(8 + theta.size * 8)},
         "gpu_launches": len(prof) // max(args.steps, 1) * args.steps,
         "clocks": clk, "cpu_baseline": None,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
+    S.release()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

@@ -291,6 +291,62 @@ tcx_status tcx_shard_buffers(const tcx_circuit* circ, const tcx_pauli* pauli, in
                              int32_t want_grad, void* ws, void** psi, void** lambda,
                              int64_t* local_amps);
 
+/* ---- Library-owned communicator for the sharded state (north_star "gates on
+ * global qubits are handled by NCCL all-to-all qubit swaps over NVLink"; PAPER.md:1788 outlook,
+ * "distributed quantum circuit simulation").  tcx_grad_sharded runs the whole program of
+ * tcx_shard_program for this process's rank(s): every compute step in the library's kernels,
+ * every EXCHANGE in the library's transport on its own streams (ordered after / before the
+ * caller's stream with events), then the sum of E / grad over ranks, so E and grad come back
+ * complete (identical on every rank).
+ *   TCX_COMM_NCCL     one process per GPU; tcx_comm_init bootstraps an NCCL communicator from
+ *                     an ncclUniqueId (NCCL_UNIQUE_ID_BYTES = 128 bytes, made by
+ *                     tcx_comm_unique_id on one rank and broadcast by the caller, e.g. with
+ *                     torch.distributed).  libnccl.so.2 is resolved at run time (the copy
+ *                     already loaded in the process first).  The exchange: XOR-pairwise steps,
+ *                     grouped ncclSend straight from the contiguous [B][G][C] blocks (no pack
+ *                     kernel) and ncclRecv into two staging chunks (TCX_XCHG_CHUNK_MB, default
+ *                     256 MiB each, inside ws) copied into place on a second stream while the
+ *                     next chunk is on the wire; E/grad: ncclAllReduce(sum).
+ *   TCX_COMM_VIRTUAL  all 2^g ranks in this process on the current device (one-GPU runs and
+ *                     parity tests): ws holds every rank's workspace; the exchange is an
+ *                     in-place swap kernel (no staging); E/grad: fixed-order sum over ranks.
+ *   TCX_COMM_HOST     tests with several processes on one device: each exchange goes block ->
+ *                     pinned host -> fn -> block synchronously; fn(user, peer, send, recv,
+ *                     bytes) must send `bytes` host bytes to rank `peer` and receive as many
+ *                     from it (return 0 on success); E/grad: recursive doubling through fn.
+ * A comm is bound to the device current at init; it must not be used by two calls at once.
+ * Errors: TCX_E_INVALID (world not a power of two in [1, 64], rank out of range, world !=
+ * 2^global_bits of the circuit, workspace too small), TCX_E_NCCL (library missing, NCCL or
+ * callback failure). */
+typedef struct tcx_comm tcx_comm;
+enum { TCX_COMM_VIRTUAL = 0, TCX_COMM_NCCL = 1, TCX_COMM_HOST = 2 };
+typedef int32_t (*tcx_host_exchange_fn)(void* user, int32_t peer, const void* send_host,
+                                        void* recv_host, size_t bytes);
+tcx_status tcx_comm_unique_id(void* nccl_unique_id_out /* 128 bytes */);
+tcx_status tcx_comm_init(const void* nccl_unique_id, int32_t world, int32_t rank, tcx_comm** out);
+tcx_status tcx_comm_init_virtual(int32_t world, tcx_comm** out);
+tcx_status tcx_comm_init_host(int32_t world, int32_t rank, tcx_host_exchange_fn fn, void* user,
+                              tcx_comm** out);
+tcx_status tcx_comm_info(const tcx_comm* comm, int32_t* kind, int32_t* world, int32_t* rank);
+void tcx_comm_free(tcx_comm* comm);
+/* Device workspace for one tcx_grad_sharded (want_grad = 1) / tcx_expect_sharded call with
+ * this comm: per local rank the psi (+ lambda) [B][2^(n-g)] complex buffers and partials,
+ * plus the staging chunks (NCCL).  A circuit with global_bits = 0 and a world of 1 is the
+ * ordinary single-GPU program (then the all-reduce is a no-op). */
+tcx_status tcx_sharded_workspace_bytes(const tcx_circuit* circ, const tcx_pauli* pauli,
+                                       const tcx_comm* comm, int64_t B, int32_t want_grad,
+                                       size_t* bytes);
+/* E[b] and grad[b][p] of the full (2^n-amplitude) state for theta rows b < B; theta: device
+ * [B][n_params] float64, identical on every rank; E: device [B], grad: device [B][n_params]
+ * float64, complete on return (summed over ranks).  Enqueued on cuda_stream except the host
+ * transport, which synchronizes it. */
+tcx_status tcx_grad_sharded(const tcx_circuit* circ, const tcx_pauli* pauli, tcx_comm* comm,
+                            const double* theta, int64_t B, double* E, double* grad, void* ws,
+                            size_t ws_bytes, void* cuda_stream);
+tcx_status tcx_expect_sharded(const tcx_circuit* circ, const tcx_pauli* pauli, tcx_comm* comm,
+                              const double* theta, int64_t B, double* E, void* ws,
+                              size_t ws_bytes, void* cuda_stream);
+
 /* Per-launch device timing (bench.py roofline).  When enabled on the calling thread,
  * every kernel a compute entry enqueues is bracketed by CUDA events recorded on the
  * call's stream.  tcx_profile_read waits for the recorded events, returns up to cap
@@ -298,7 +354,10 @@ tcx_status tcx_shard_buffers(const tcx_circuit* circ, const tcx_pauli* pauli, in
  * ALGORITHMIC floating-point operations and HBM bytes. */
 typedef struct {
     int32_t phase;   /* 0 materialize, 1 forward pass, 2 lambda pass, 3 backward pass,
-                        4 finalize, 5 fused single pass (forward + lambda + backward) */
+                        4 finalize, 5 fused single pass (forward + lambda + backward),
+                        6 dense block, 7 dense block backward, 8 sharded-state exchange
+                        (bytes = data that changes rank; virtual ranks: HBM read + write),
+                        9 last forward pass fused with lambda and its backward */
     int32_t index;   /* pass / lambda-unit index */
     float ms;
     float pad;

@@ -291,190 +291,6 @@ __global__ void __launch_bounds__(128) dense_fwd_tc_kernel(const DenseArgs a) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(N));
 }
 
-// ---- warp-specialised variant: 4 producer warps, 4 epilogue warps, 2-stage A ring and a
-// double-buffered TMEM accumulator, so loads of tile i+1, the MMA of tile i and the stores of
-// tile i-1 overlap inside one CTA (one CTA per SM).  Producers keep two tiles of loads in
-// registers (software pipeline); thread 0 of the producers issues the MMAs and commits to
-// `stage_free` (A stage may be overwritten) and `acc_full` (accumulator ready); epilogue
-// threads read their TMEM lane, arrive on `acc_free` and scatter.
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-
-template <int K>
-__global__ void __launch_bounds__(256, 1) dense_fwd_tc_ws_kernel(const DenseArgs a) {
-  static_assert(K == 5, "tensor-core dense blocks are k = 5");
-  constexpr int D = 1 << K, KD = 2 * D, N = 2 * D, M = 128;
-  constexpr int A_BYTES = M * KD * 4, B_BYTES = N * KD * 4;
-  constexpr uint32_t IDESC = umma_idesc_tf32(M, N);
-  extern __shared__ __align__(1024) unsigned char tsm[];
-  unsigned char* base = tsm + ((1024 - (smem_u32(tsm) & 1023)) & 1023);
-  unsigned char* sA = base;                    // [2 stages][hi, lo][A_BYTES]
-  unsigned char* sBh = sA + 4 * A_BYTES;
-  unsigned char* sBl = sBh + B_BYTES;
-  __shared__ uint64_t acc_full[2], acc_free[2], stage_free[2];
-  __shared__ uint32_t s_tmem;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t b = a.b0 + blockIdx.y;
-  if (warp == 0) {  // two accumulators of N fp32 columns
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(&s_tmem)),
-                 "r"(2 * N));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  if (tid == 0) {
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_free[i], 128);
-      mbar_init(&stage_free[i], 1);
-    }
-  }
-  {
-    const Cx<float>* U = reinterpret_cast<const Cx<float>*>(a.U) + b * a.u_stride;
-    for (int e = tid; e < N * KD; e += blockDim.x) {
-      const int n = e / KD, k = e % KD;
-      const int i = n % D, j = k % D;
-      const Cx<float> u = U[i * D + j];
-      float v;
-      if (n < D) v = k < D ? u.x : -u.y;
-      else v = k < D ? u.y : u.x;
-      const float h = tf32_hi(v);
-      *reinterpret_cast<float*>(sBh + sw128_off(n, k, N)) = h;
-      *reinterpret_cast<float*>(sBl + sw128_off(n, k, N)) = v - h;
-    }
-  }
-  fence_async_smem();
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = s_tmem;
-  int bits[K];
-#pragma unroll
-  for (int i = 0; i < K; ++i) bits[i] = a.bits[i];
-  const bool rowpair = bits[0] == 0;
-  const int64_t Nst = 1ll << a.n;
-  const int64_t ncols = Nst >> K;
-  const int64_t ntiles = (ncols + M - 1) / M;
-  const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  float* psi = reinterpret_cast<float*>(reinterpret_cast<Cx<float>*>(a.psi) + b * Nst);
-
-  if (warp < 4) {  // ---------------- producers (+ MMA issue by thread 0)
-    const int cp = tid & 63, hh = tid >> 6;
-    auto load = [&](int64_t tile, float4* w) {
-      const int64_t c = rowpair ? tile * M + tid : tile * M + 2 * cp;
-      const bool ok = c < ncols;
-      const uint64_t bs = dense_insert<K>(ok ? (uint64_t)c : 0ull, bits);
-#pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const int j = rowpair ? 2 * q : 16 * hh + q;
-        if (a.init)
-          w[q] = make_float4((ok && c == 0 && j == 0) ? 1.f : 0.f, 0.f, 0.f, 0.f);
-        else
-          w[q] = ok ? *reinterpret_cast<const float4*>(psi + 2 * (bs | dense_off<K>(j, bits)))
-                    : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-    };
-    auto step = [&](int64_t i, const float4* w) {
-      const int s = (int)(i & 1);
-      if (i >= 2) mbar_wait(&stage_free[s], (uint32_t)(((i >> 1) - 1) & 1));
-      unsigned char* sAh = sA + (2 * s) * A_BYTES;
-      unsigned char* sAl = sAh + A_BYTES;
-      if (rowpair) {
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const float4 p0 = w[2 * u], p1 = w[2 * u + 1];
-          put4(sAh, sAl, tid, 4 * u, p0.x, p0.z, p1.x, p1.z);
-          put4(sAh, sAl, tid, D + 4 * u, p0.y, p0.w, p1.y, p1.w);
-        }
-      } else {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float4 p0 = w[4 * u], p1 = w[4 * u + 1], p2 = w[4 * u + 2], p3 = w[4 * u + 3];
-          const int k0 = 16 * hh + 4 * u;
-          put4(sAh, sAl, 2 * cp, k0, p0.x, p1.x, p2.x, p3.x);
-          put4(sAh, sAl, 2 * cp, D + k0, p0.y, p1.y, p2.y, p3.y);
-          put4(sAh, sAl, 2 * cp + 1, k0, p0.z, p1.z, p2.z, p3.z);
-          put4(sAh, sAl, 2 * cp + 1, D + k0, p0.w, p1.w, p2.w, p3.w);
-        }
-      }
-      fence_async_smem();
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (tid == 0) {
-        if (i >= 2) mbar_wait(&acc_free[s], (uint32_t)(((i >> 1) - 1) & 1));
-        tc_fence_after();
-        const uint32_t aH = smem_u32(sAh), aL = smem_u32(sAl), bH = smem_u32(sBh), bL = smem_u32(sBl);
-        const uint32_t d = tmem + (uint32_t)(s * N);
-#pragma unroll
-        for (int k = 0; k < KD / 8; ++k) {
-          const uint32_t ao = (k >> 2) * (M * 128) + (k & 3) * 32;
-          const uint32_t bo = (k >> 2) * (N * 128) + (k & 3) * 32;
-          umma_tf32(d, umma_desc_sw128(aH + ao, 1024), umma_desc_sw128(bH + bo, 1024), IDESC, k > 0);
-          umma_tf32(d, umma_desc_sw128(aL + ao, 1024), umma_desc_sw128(bH + bo, 1024), IDESC, 1);
-          umma_tf32(d, umma_desc_sw128(aH + ao, 1024), umma_desc_sw128(bL + bo, 1024), IDESC, 1);
-        }
-        umma_commit(&stage_free[s]);
-        umma_commit(&acc_full[s]);
-      }
-    };
-    float4 w0[16], w1[16];
-    if (my_tiles > 0) load(blockIdx.x, w0);
-    for (int64_t i = 0; i < my_tiles; i += 2) {
-      if (i + 1 < my_tiles) load(blockIdx.x + (i + 1) * gridDim.x, w1);
-      step(i, w0);
-      if (i + 1 >= my_tiles) break;
-      if (i + 2 < my_tiles) load(blockIdx.x + (i + 2) * gridDim.x, w0);
-      step(i + 1, w1);
-    }
-  } else {  // ----------------------- epilogue
-    const int et = tid - 128, ew = warp - 4;
-    const bool odd = lane & 1;
-    for (int64_t i = 0; i < my_tiles; ++i) {
-      const int s = (int)(i & 1);
-      const int64_t tile = blockIdx.x + i * gridDim.x;
-      mbar_wait(&acc_full[s], (uint32_t)((i >> 1) & 1));
-      tc_fence_after();
-      float o[N];
-      const uint32_t trow = tmem + ((uint32_t)(ew * 32) << 16) + (uint32_t)(s * N);
-#pragma unroll
-      for (int h = 0; h < N / 32; ++h) tmem_ld32(trow + h * 32, o + 32 * h);
-      tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(&acc_free[s]);
-      const int64_t c = tile * M + et;
-      if (rowpair) {
-        const bool ok = c < ncols;
-        const uint64_t bs = dense_insert<K>(ok ? (uint64_t)c : 0ull, bits);
-        if (ok) {
-#pragma unroll
-          for (int q = 0; q < 16; ++q)
-            *reinterpret_cast<float4*>(psi + 2 * (bs | dense_off<K>(2 * q, bits))) =
-                make_float4(o[2 * q], o[D + 2 * q], o[2 * q + 1], o[D + 2 * q + 1]);
-        }
-      } else {
-        const int64_t ce = c & ~1ll;
-        const bool ok = ce < ncols;
-        const uint64_t bs = dense_insert<K>(ok ? (uint64_t)ce : 0ull, bits);
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const float lo_r = o[q], lo_i = o[D + q], hi_r = o[16 + q], hi_i = o[D + 16 + q];
-          const float sr = __shfl_xor_sync(0xffffffffu, odd ? lo_r : hi_r, 1);
-          const float si = __shfl_xor_sync(0xffffffffu, odd ? lo_i : hi_i, 1);
-          const int j = odd ? 16 + q : q;
-          const float4 v = odd ? make_float4(sr, si, hi_r, hi_i) : make_float4(lo_r, lo_i, sr, si);
-          if (ok) *reinterpret_cast<float4*>(psi + 2 * (bs | dense_off<K>(j, bits))) = v;
-        }
-      }
-    }
-  }
-  __syncthreads();
-  if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * N));
-}
-
-inline constexpr int dense_tc_ws_smem(int K) {  // 2 A stages (hi, lo) + B (hi, lo) + align
-  return 4 * 128 * (2 << K) * 4 + 2 * (2 << K) * (2 << K) * 4 + 1024;
-}
-
 inline constexpr int dense_tc_smem(int K) {
   return 2 * 128 * (2 << K) * 4 + 2 * (2 << K) * (2 << K) * 4 + 1024;
 }

@@ -95,12 +95,12 @@ struct PassArgs {
 };
 
 struct SmemLayout {
-  int xb_psi, xb_lam, mats, wacc, cacc, stages, red, total;
+  int xb_psi, xb_lam, mats, wacc, cacc, stages, red, pb, total;
 };
 TCX_HD inline int al16(int x) { return (x + 15) & ~15; }
 TCX_HD inline SmemLayout smem_layout(int t, int h, int realsz, int mat_count,
                                      int max_stage_acc, int acc_count, int nstages, bool two,
-                                     int nsub = 1) {
+                                     int nsub = 1, bool pipe = false) {
   // nsub lock-stepped sub-tiles per CTA (JIT kernels): one exchange buffer each
   SmemLayout L;
   int off = 0;
@@ -120,6 +120,14 @@ TCX_HD inline SmemLayout smem_layout(int t, int h, int realsz, int mat_count,
   off = al16(off + (int)sizeof(KStage) * nstages);
   L.red = off;
   off = al16(off + 8 * 32);
+  // pipelined TMA passes: the next tile (psi, and lambda in two-state kernels) lands here
+  // while this one is computed (128-byte aligned TMA destination)
+  L.pb = 0;
+  if (pipe) {
+    off = (off + 127) & ~127;
+    L.pb = off;
+    off += (two ? 2 : 1) * (csz << t);
+  }
   L.total = off;
   return L;
 }

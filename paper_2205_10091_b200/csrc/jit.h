@@ -14,5 +14,13 @@ std::string jit_key_lambda(uint64_t pauli_hash, int unit);
 // compile (or fetch from the disk cache) the kernels not yet built
 bool jit_build(Plan& P, const std::vector<std::string>& keys, std::string& err);
 std::string jit_source(const Plan& P, const std::string& key);  // generated CUDA C++
+// drop a built kernel and its disk-cache entry (the driver rejected the cubin): the next
+// jit_build of the key compiles it afresh
+void jit_evict(Plan& P, const std::string& key);
 std::string jit_kernel_name(const std::string& key);
+// software-pipelined TMA tiles (Plan::jit_pipe) for pass p's kernel with (bwd = two-state)
+// or without the backward: on when the plan asks for it, the window is a TMA box and the
+// prefetch buffer still fits the 227 KB of shared memory
+struct PassInfo;
+bool jit_pipe_on(const Plan& P, const PassInfo& p, bool bwd);
 }  // namespace tcx

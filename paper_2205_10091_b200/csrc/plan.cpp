@@ -307,6 +307,7 @@ struct Scheduler {
   // the greedy choice to the end of the schedule and the one finishing in the fewest passes
   // wins (ties: more work now).
   bool lookahead = false;
+  bool tma_ok(uint64_t W) const { return tma_dims(nl, W, P.dtype == TCX_C128).rank > 0; }
   uint64_t choose_window() {
     std::vector<std::pair<double, uint64_t>> cand;
     uint64_t W0 = candidates(&cand);
@@ -328,7 +329,7 @@ struct Scheduler {
     for (size_t k = 0; k < K; ++k) {
       uint64_t W = cand[k].second;
       int passes = 0;
-      bool ok = true;
+      bool ok = true, finished = false;
       for (;;) {
         std::vector<int> list;
         closure(W, &list);
@@ -339,12 +340,16 @@ struct Scheduler {
         for (int i : list) done[i] = 1;
         while (first < (int)P.ops.size() && done[first]) first++;
         ++passes;
-        if (first >= (int)P.ops.size() || passes >= bestp) break;
+        finished = first >= (int)P.ops.size();
+        if (finished || passes >= bestp) break;
         W = candidates(nullptr);
       }
       done = done0;
       first = first0;
-      if (ok && passes < bestp) {
+      // ties in the pass count go to windows whose tile is a TMA box (<= 5 contiguous index
+      // runs): those passes move tiles with cp.async.bulk.tensor (and prefetch the next one)
+      if (ok && finished &&
+          (passes < bestp || (passes == bestp && tma_ok(cand[k].second) && !tma_ok(bestW)))) {
         bestp = passes;
         bestW = cand[k].second;
       }
@@ -908,12 +913,17 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
   P.tpc = (int)std::min<int64_t>(64, std::max<int64_t>(1, P.tiles / 32));
   // two lock-stepped sub-tiles (512 threads) share one instruction stream in the JIT
   // kernels when tiles pair up and a sub-tile has whole warps
+  // software-pipelined TMA tiles (prefetch of tile i+1 into its own buffer while tile i is
+  // computed; the store of tile i drains while tile i+1 runs)
+  P.jit_pipe = getenv("TCX_JIT_PIPE") ? atoi(getenv("TCX_JIT_PIPE")) != 0 : false;
   P.jit_nsub = 1;  // 2 = lock-stepped sub-tiles (measured slower with FFMA2 code; opt-in via TCX_JIT_NSUB)
   if (const char* e = getenv("TCX_JIT_NSUB"))
     if (atoi(e) == 2 && P.tpc % 2 == 0 && P.h >= 5) P.jit_nsub = 2;
   // ---- lower
   int pos[kMaxQubits];
   for (int q = 0; q < n; ++q) pos[q] = n - 1 - q;  // PAPER.md:249 qubit 0 = MSB
+  if ((int)P.init_pos.size() == n)  // sharded layout search (tcx_circuit_build)
+    for (int q = 0; q < n; ++q) pos[q] = P.init_pos[q];
   Lowerer L(P);
   auto payload_copy_raw = [&](int64_t off, int elems) {  // complex elements, no checks
     int64_t at = (int64_t)P.fixed.size() / 2;

@@ -159,6 +159,7 @@ struct DeviceTables;
 
 struct JitKernel {      // NVRTC-compiled specialisation (jit.cpp)
   std::string key, name;
+  std::string cache_key;  // disk cache entry it came from / went to ("" = none)
   std::vector<char> cubin;
 };
 
@@ -169,6 +170,7 @@ struct Plan {
   int max_ops_per_pass = 0;
   int gbits = 0, nloc = 0;       // sharded state: global index bits, local bits (= n if not)
   int nseg = 1;                  // sharded: layouts separated by global<->top-local exchanges
+  std::vector<int> init_pos;     // sharded: initial physical bit of each qubit (empty: n-1-q)
   std::vector<tcx_gate> gates;  // validated input (decode)
   std::vector<double> mats_in;  // input payloads
   std::vector<double> fixed;    // complex (re, im) payloads referenced by ops
@@ -190,6 +192,7 @@ struct Plan {
   int64_t tiles = 1;             // 2^(n - t)
   int tpc = 1;                   // tiles per CTA (depends on the tile count only, never on B)
   int jit_nsub = 1;              // lock-stepped sub-tiles per CTA in JIT kernels
+  bool jit_pipe = false;         // JIT TMA passes prefetch the next tile / defer store waits
 
   uint64_t init_hmask = 0;         // leading H gates folded into the initial state (bits)
   uint64_t fold_mask = 0;          // bits whose leading U1 op is folded into the initial state
@@ -210,6 +213,8 @@ struct Plan {
 
   std::mutex mu;
   std::map<uint64_t, std::shared_ptr<Binding>> bindings;  // keyed by Pauli::hash
+  std::map<uint64_t, uint64_t> binding_use;  // Pauli::hash -> last use (LRU eviction)
+  uint64_t use_clock = 0;
   std::map<int, std::shared_ptr<DeviceTables>> dev;
 };
 

@@ -17,6 +17,8 @@
 #include <memory>
 #include <string>
 #include <type_traits>
+#include <atomic>
+#include <thread>
 
 #include "jit.h"
 #include "kernels.cuh"
@@ -309,6 +311,7 @@ struct DeviceTables {
   DevBuf dblocks, dgates, dpblocks;  // dense k-qubit blocks (dense.cuh)
   std::map<std::string, CUfunction> jit;   // key (jit.h)
   std::map<std::string, size_t> jit_smem;  // dynamic smem opted in per function
+  std::map<std::string, CUmodule> jit_mod;  // key -> its module (unloaded on eviction)
   std::vector<CUmodule> modules;           // loaded JIT modules (unloaded with the plan)
   ~DeviceTables();
 };
@@ -461,13 +464,19 @@ tcx_status jit_function(Plan& P, DeviceTables* DT, const std::string& key, CUfun
   CUDA_TRY(cudaFree(0));  // primary context current on this thread
   CUmodule m;
   CUfunction fn;
+  if (D.moduleLoadData(&m, P.jit.at(key).cubin.data()) != CUDA_SUCCESS) {
+    // a stale or damaged cache entry: drop it, compile afresh, and try once more
+    jit_evict(P, key);
+    if (!jit_build(P, {key}, err)) return fail(TCX_E_CUDA, err);
+    if (D.moduleLoadData(&m, P.jit.at(key).cubin.data()) != CUDA_SUCCESS)
+      return fail(TCX_E_CUDA, "cuModuleLoadData failed for " + P.jit.at(key).name);
+  }
   const JitKernel& k = P.jit.at(key);
-  if (D.moduleLoadData(&m, k.cubin.data()) != CUDA_SUCCESS)
-    return fail(TCX_E_CUDA, "cuModuleLoadData failed for " + k.name);
   if (D.moduleGetFunction(&fn, m, k.name.c_str()) != CUDA_SUCCESS)
     return fail(TCX_E_CUDA, "cuModuleGetFunction failed for " + k.name);
   std::lock_guard<std::mutex> lk(P.mu);
   DT->modules.push_back(m);
+  DT->jit_mod[key] = m;
   DT->jit[key] = fn;
   DT->jit_smem[key] = 0;
   *f = fn;
@@ -477,6 +486,10 @@ tcx_status jit_function(Plan& P, DeviceTables* DT, const std::string& key, CUfun
 // Compile every specialised kernel a call of this kind needs, in parallel, before launching.
 // grad with one lambda unit: the last forward pass, lambda = H psi and that pass's backward
 // run as one kernel per tile (no store / reload of psi and lambda in between)
+int jit_key_pass_index(const std::string& key) {  // "p<pass>k<km>"
+  return atoi(key.c_str() + 1);
+}
+
 bool fuse_last_of(const Plan& P, int kind, bool mega, const Binding* Bd) {
   static const bool no_fuse = getenv("TCX_NO_FUSE_LAST") != nullptr;
   return !no_fuse && kind == 1 && !mega && P.gbits == 0 && P.dblocks.empty() &&
@@ -512,6 +525,51 @@ struct BindDev {
   KPTerm* pterms;
 };
 
+// Bindings (lambda schedule, device term tables, per-unit JIT kernels) of at most this many
+// Hamiltonians stay cached per plan; beyond it the least recently used one is dropped.
+constexpr size_t kMaxBindings = 64;
+
+void evict_binding_locked(Plan& P, uint64_t hash) {  // P.mu held
+  P.bindings.erase(hash);
+  P.binding_use.erase(hash);
+  const std::string pre = jit_key_lambda(hash, 0).substr(0, 18);  // "L<16 hex>u"
+  {
+    std::lock_guard<std::mutex> jl(P.jit_mu);
+    for (auto it = P.jit.begin(); it != P.jit.end();)
+      it = it->first.compare(0, pre.size(), pre) == 0 ? P.jit.erase(it) : std::next(it);
+  }
+  bool synced = false;
+  Drv& D = drv();
+  for (auto& kv : P.dev) {
+    DeviceTables* DT = kv.second.get();
+    for (auto it = DT->jit.begin(); it != DT->jit.end();) {
+      if (it->first.compare(0, pre.size(), pre) != 0) {
+        ++it;
+        continue;
+      }
+      auto mi = DT->jit_mod.find(it->first);
+      if (mi != DT->jit_mod.end()) {
+        if (!synced) {  // its kernels may still be queued: unload only once the devices idle
+          int cur = 0;
+          cudaGetDevice(&cur);
+          for (auto& d2 : P.dev) {
+            cudaSetDevice(d2.first);
+            cudaDeviceSynchronize();
+          }
+          cudaSetDevice(cur);
+          synced = true;
+        }
+        if (D.ok) D.moduleUnload(mi->second);
+        DT->modules.erase(std::remove(DT->modules.begin(), DT->modules.end(), mi->second),
+                          DT->modules.end());
+        DT->jit_mod.erase(mi);
+      }
+      DT->jit_smem.erase(it->first);
+      it = DT->jit.erase(it);
+    }
+  }
+}
+
 tcx_status binding_for(Plan& P, const tcx_pauli* H, std::shared_ptr<Binding>& out, BindDev* dv) {
   {
     std::lock_guard<std::mutex> lk(P.mu);
@@ -526,6 +584,20 @@ tcx_status binding_for(Plan& P, const tcx_pauli* H, std::shared_ptr<Binding>& ou
       out = it->second;
     else
       P.bindings[H->p.hash] = out = b;
+  }
+  {
+    std::lock_guard<std::mutex> lk(P.mu);
+    P.binding_use[H->p.hash] = ++P.use_clock;
+    while (P.bindings.size() > kMaxBindings) {
+      uint64_t victim = 0, oldest = UINT64_MAX;
+      for (auto& u : P.binding_use)
+        if (u.first != H->p.hash && u.second < oldest) {
+          oldest = u.second;
+          victim = u.first;
+        }
+      if (oldest == UINT64_MAX) break;
+      evict_binding_locked(P, victim);
+    }
   }
   if (!out->xmask_ok) return fail(TCX_E_UNSUPPORTED, out->err);
   if (dv) {
@@ -681,25 +753,6 @@ bool dense_tc_on(int K) {
   }();
   return mode != 0 && K == 5;
 }
-int dense_tc_variant() {  // 1: one role per thread, 2 CTAs per SM; 2: warp-specialised
-  static const int v = [] {
-    const char* e = getenv("TCX_DENSE_TC_WS");
-    return e ? atoi(e) : 1;
-  }();
-  return v;
-}
-template <int K>
-cudaError_t dense_fwd_tc_ws_launch(DenseArgs& a, int64_t rows, cudaStream_t st) {
-  const int sm = dense_tc_ws_smem(K);
-  cudaError_t e = cudaFuncSetAttribute(dense_fwd_tc_ws_kernel<K>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  if (e != cudaSuccess) return e;
-  const int64_t ncols = ((int64_t)1 << a.n) >> K;
-  const int64_t tiles = (ncols + 127) / 128;
-  const int64_t gx = std::max<int64_t>(1, std::min<int64_t>(tiles, std::max<int64_t>(1, 148 / rows)));
-  dense_fwd_tc_ws_kernel<K><<<dim3((unsigned)gx, (unsigned)rows), 256, sm, st>>>(a);
-  return cudaGetLastError();
-}
 template <int K>
 cudaError_t dense_fwd_tc_launch(DenseArgs& a, int64_t rows, cudaStream_t st) {
   const int sm = dense_tc_smem(K);
@@ -715,8 +768,7 @@ cudaError_t dense_fwd_tc_launch(DenseArgs& a, int64_t rows, cudaStream_t st) {
 template <typename Real>
 cudaError_t dense_fwd(int K, DenseArgs& a, int64_t rows, cudaStream_t st) {
   if (sizeof(Real) == 4 && dense_tc_on(K))
-    return dense_tc_variant() == 2 ? dense_fwd_tc_ws_launch<5>(a, rows, st)
-                                   : dense_fwd_tc_launch<5>(a, rows, st);
+    return dense_fwd_tc_launch<5>(a, rows, st);
   switch (K) {
     case 1: dense_fwd_launch<Real, 1>(a, rows, st); break;
     case 2: dense_fwd_launch<Real, 2>(a, rows, st); break;
@@ -955,8 +1007,9 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
             a.use_tma = (wl.lam == 0 || encode_tmap(a.tmap[1], a.lam, td, P.nloc, B)) ? 1 : 0;
           if (!(a.mode & (M_LOAD_PSI | M_LOAD_LAM | M_STORE_PSI | M_STORE_LAM))) a.use_tma = 0;
         }
+        const bool pipe = jkey[0] == 'p' && jit_pipe_on(P, P.passes[jit_key_pass_index(jkey)], two);
         const SmemLayout LJ = smem_layout(a.t, a.h, rs, a.mat_count, a.max_stage_acc,
-                                          (a.mode & M_BWD) ? a.acc_count : 0, a.nstages, two, ns);
+                                          (a.mode & M_BWD) ? a.acc_count : 0, a.nstages, two, ns, pipe);
         if (LJ.total > 227 * 1024 - 1280)
           return fail(TCX_E_UNSUPPORTED, "JIT pass needs too much shared memory");
         if (LJ.total > 48 * 1024 && (size_t)LJ.total > DT->jit_smem[jkey]) {
@@ -990,7 +1043,7 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
     std::string jkey;
     if (P.jit_on) {
       const bool fwdk = (a.mode & (M_FWD | M_LAMBDA)) != 0, bwdk = (a.mode & M_BWD) != 0;
-      if (phase == 1 || phase == 3 || phase == 5)
+      if (phase == 1 || phase == 3 || phase == 5 || phase == 9)
         jkey = jit_key_pass(index, (fwdk && bwdk) ? 2 : (bwdk ? 1 : 0));
       else if (phase == 2 && Bd)
         jkey = jit_key_lambda(Bd->hash, index);
@@ -1085,7 +1138,8 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
       double fl = pass_flops(P, p, false);
       if (last && kind != K_STATE) fl += lambda_flops(*Bd, Bd->units[0]);
       if (last && fuse_last) fl += pass_flops(P, p, true);
-      if ((s = launch(a, 1, pi, fl))) return s;
+      // the fused last pass (forward + lambda + backward) is its own profiling class
+      if ((s = launch(a, (last && fuse_last) ? 9 : 1, pi, fl))) return s;
     }
     if (kind != K_STATE) {
       for (int u = sharded ? 0 : 1; u < EU; ++u) {
@@ -1245,6 +1299,43 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
   return TCX_OK;
 }
 
+// The fixed step list of a sharded program (identical on every rank): materialise, forward
+// passes with an EXCHANGE between segments, lambda units (those flipping global qubits run
+// after an exchange), backward passes mirrored, finalise.
+std::vector<tcx_shard_step> shard_program(const Plan& P, const Binding& Bdr, bool want_grad) {
+  const Binding* Bd = &Bdr;
+  std::vector<tcx_shard_step> v;
+  auto add = [&](int k, int a) { v.push_back({k, a}); };
+  const int nP = (int)P.passes.size();
+  add(TCX_STEP_MATERIALIZE, 0);
+  for (int p = 0; p < nP; ++p) {
+    if (p > 0 && P.passes[p].seg != P.passes[p - 1].seg) add(TCX_STEP_EXCHANGE, 1);
+    add(TCX_STEP_FWD, p);
+  }
+  const int x = want_grad ? 3 : 1;  // exchange psi (+ lambda once it exists)
+  bool any_lam = false;
+  for (int u = 0; u < (int)Bd->units.size(); ++u)
+    if (!Bd->units[u].swapped) {
+      add(TCX_STEP_LAMBDA, u);
+      any_lam = true;
+    }
+  bool sw = false;
+  for (int u = 0; u < (int)Bd->units.size(); ++u)
+    if (Bd->units[u].swapped) {
+      if (!sw) add(TCX_STEP_EXCHANGE, any_lam ? x : 1);
+      sw = true;
+      add(TCX_STEP_LAMBDA, u);
+    }
+  if (sw && want_grad) add(TCX_STEP_EXCHANGE, x);  // back to the backward's layout
+  if (want_grad)
+    for (int p = nP - 1; p >= 0; --p) {
+      add(TCX_STEP_BWD, p);
+      if (p > 0 && P.passes[p].seg != P.passes[p - 1].seg) add(TCX_STEP_EXCHANGE, 3);
+    }
+  add(TCX_STEP_FINALIZE, 0);
+  return v;
+}
+
 }  // namespace
 
 // ================================================================== C ABI
@@ -1273,6 +1364,57 @@ tcx_status tcx_circuit_build(int32_t n_qubits, int32_t n_params, const tcx_gate*
   if (s) {
     delete c;
     return fail(s, err);
+  }
+  if (c->plan.gbits > 0 && !getenv("TCX_SHARD_NO_LAYOUT_SEARCH")) {
+    // Sharded layout search.  The exchange always swaps the g global bits (qubits 0..g-1,
+    // the state's top bits) with the g top LOCAL bits, so which qubits sit in those bits
+    // decides how often the two sets must trade places.  Try every contiguous run of g
+    // qubits there (the rest keep paper order below them) and keep the plan with the fewest
+    // segments (exchanges), then the fewest passes.  HEA: the run at the far end of the
+    // CNOT ladder lets the light cone sweep a whole band of layers per segment.
+    const int n = n_qubits, g = c->plan.gbits, nl = n - g;
+    std::vector<int> cands;
+    for (int b = g; b + g <= n; ++b) cands.push_back(b);
+    std::vector<tcx_circuit*> built(cands.size(), nullptr);
+    std::atomic<int> next{0};
+    auto work = [&] {
+      for (int i = next++; i < (int)cands.size(); i = next++) {
+        tcx_circuit* t = new (std::nothrow) tcx_circuit();
+        if (!t) continue;
+        std::vector<int> pos(n);
+        for (int q = 0; q < g; ++q) pos[q] = n - 1 - q;                  // global: top bits
+        for (int j = 0; j < g; ++j) pos[cands[i] + j] = nl - 1 - j;      // top local bits
+        int bit = nl - g - 1;
+        for (int q = g; q < n; ++q)
+          if (q < cands[i] || q >= cands[i] + g) pos[q] = bit--;
+        t->plan.init_pos = pos;
+        std::string e2;
+        tcx_status s2;
+        try {
+          s2 = build_plan(n_qubits, n_params, gates, n_gates, matrices, n_matrix_elems, dtype,
+                          opts, t->plan, e2);
+        } catch (...) {
+          s2 = TCX_E_OOM;
+        }
+        if (s2) {
+          delete t;
+          t = nullptr;
+        }
+        built[i] = t;
+      }
+    };
+    const int nth = std::max(1, std::min<int>((int)cands.size(),
+                                              (int)std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    for (int i = 0; i < nth; ++i) th.emplace_back(work);
+    for (auto& x : th) x.join();
+    for (auto*& t : built) {
+      if (!t) continue;
+      const Plan &A = t->plan, &Bp = c->plan;
+      if (A.nseg < Bp.nseg || (A.nseg == Bp.nseg && A.passes.size() < Bp.passes.size())) std::swap(c, t);
+      delete t;
+      t = nullptr;
+    }
   }
   if (!opts || opts->jit >= 0) {
     std::string why;
@@ -1598,35 +1740,7 @@ tcx_status tcx_shard_program(const tcx_circuit* circ, const tcx_pauli* pauli, in
   std::shared_ptr<Binding> Bd;
   tcx_status s = binding_for(P, pauli, Bd, nullptr);
   if (s) return s;
-  std::vector<tcx_shard_step> v;
-  auto add = [&](int k, int a) { v.push_back({k, a}); };
-  const int nP = (int)P.passes.size();
-  add(TCX_STEP_MATERIALIZE, 0);
-  for (int p = 0; p < nP; ++p) {
-    if (p > 0 && P.passes[p].seg != P.passes[p - 1].seg) add(TCX_STEP_EXCHANGE, 1);
-    add(TCX_STEP_FWD, p);
-  }
-  const int x = want_grad ? 3 : 1;  // exchange psi (+ lambda once it exists)
-  bool any_lam = false;
-  for (int u = 0; u < (int)Bd->units.size(); ++u)
-    if (!Bd->units[u].swapped) {
-      add(TCX_STEP_LAMBDA, u);
-      any_lam = true;
-    }
-  bool sw = false;
-  for (int u = 0; u < (int)Bd->units.size(); ++u)
-    if (Bd->units[u].swapped) {
-      if (!sw) add(TCX_STEP_EXCHANGE, any_lam ? x : 1);
-      sw = true;
-      add(TCX_STEP_LAMBDA, u);
-    }
-  if (sw) add(TCX_STEP_EXCHANGE, x);
-  if (want_grad)
-    for (int p = nP - 1; p >= 0; --p) {
-      add(TCX_STEP_BWD, p);
-      if (p > 0 && P.passes[p].seg != P.passes[p - 1].seg) add(TCX_STEP_EXCHANGE, 3);
-    }
-  add(TCX_STEP_FINALIZE, 0);
+  const std::vector<tcx_shard_step> v = shard_program(P, *Bd, want_grad != 0);
   *n = (int32_t)v.size();
   if (steps)
     for (int i = 0; i < std::min<int>(cap, (int)v.size()); ++i) steps[i] = v[i];
@@ -1696,35 +1810,53 @@ tcx_status tcx_launch_count(const tcx_circuit* circ, const tcx_pauli* pauli, int
                             int32_t want_grad, int32_t* launches) {
   g_err.clear();
   if (!circ || !pauli || !launches) return fail(TCX_E_INVALID, "null argument");
+  if (B <= 0) return fail(TCX_E_INVALID, "B must be > 0");
   Plan& P = const_cast<tcx_circuit*>(circ)->plan;
   std::shared_ptr<Binding> Bd;
   tcx_status s = binding_for(P, pauli, Bd, nullptr);
   if (s) return s;
   const int kind = want_grad ? K_GRAD : K_EXPECT;
   WsLayout wl = ws_layout(P, Bd.get(), B, kind, false);
-  const int64_t chunks = (B + 65534) / 65535;
-  int64_t per = 0;
-  per += P.mitems.empty() ? 0 : 1;
-  if (!P.dblocks.empty()) {
+  auto chunks = [](int64_t rows) { return (rows + 65534) / 65535; };  // grid.y chunks
+  // mirrors run(): `once` launches, `perB` per row chunk of the whole batch, `perG` per row
+  // chunk of every L2 row group (all rows when groups are off)
+  int64_t once = 0, perB = 0, perG = 0;
+  perB += P.mitems.empty() ? 0 : 1;  // materialize
+  const bool dense = !P.dblocks.empty();
+  if (dense) {
     int npb = 0;
     for (auto& d : P.dblocks) npb += d.has_param;
-    per += (P.dmat_shared > 0 ? 1 : 0) + (P.dmat_row > 0 ? 1 : 0) + (int64_t)P.dblocks.size();
+    once += P.dmat_shared > 0 ? 1 : 0;
+    perB += P.dmat_row > 0 ? 1 : 0;
+    perG += (int64_t)P.dblocks.size();  // forward blocks
     if (want_grad) {
-      int nbw = 0;
-      for (size_t i = 0; i < P.dblocks.size(); ++i) nbw += (i > 0 || P.dblocks[i].has_param) ? 1 : 0;
-      per += nbw + npb + (npb > 0 ? 1 : 0);  // backward blocks, R' sums, contributions
-      for (auto& p : P.passes) per -= p.ops.empty() ? 1 : 0;  // no backward of the E pass
+      for (size_t i = 0; i < P.dblocks.size(); ++i) {
+        const DBlock& d = P.dblocks[i];
+        if ((i == 0 || d.first) && !d.has_param) continue;  // nothing left to compute
+        perG += 1 + (d.has_param ? 1 : 0);                  // backward block (+ R' row sums)
+      }
+      perB += npb > 0 ? 1 : 0;  // dense_grad_kernel
     }
   }
-  if (wl.mega)
-    per += 1;
-  else
-    per += (int64_t)P.passes.size() + (int64_t)Bd->units.size() - 1 +
-           (want_grad ? (int64_t)P.passes.size() : 0) -
-           (fuse_last_of(P, kind, wl.mega, Bd.get()) ? 1 : 0);
-  per += 1;  // finalize
-  *launches = (int32_t)(per * chunks);
+  if (wl.mega) {
+    perB += 1;
+  } else {
+    perG += (int64_t)P.passes.size() + (int64_t)Bd->units.size() - 1 -
+            (fuse_last_of(P, kind, wl.mega, Bd.get()) ? 1 : 0);
+    if (want_grad) {
+      perG += (int64_t)P.passes.size();
+      if (dense)
+        for (auto& p : P.passes) perG -= p.ops.empty() ? 1 : 0;  // no backward of the E pass
+    }
+  }
+  perB += 1;  // finalize
+  const int64_t G = (P.l2_rows > 0 && P.gbits == 0 && !wl.mega) ? std::min<int64_t>(P.l2_rows, B) : B;
+  int64_t gchunks = 0;
+  for (int64_t g0 = 0; g0 < B; g0 += G) gchunks += chunks(std::min(B, g0 + G) - g0);
+  *launches = (int32_t)(once + perB * chunks(B) + perG * gchunks);
   return TCX_OK;
 }
 
 }  // extern "C"
+
+#include "comm.cuh"

@@ -67,7 +67,7 @@ class tcx_kernel_time(ctypes.Structure):
 
 
 PHASES = {0: "materialize", 1: "forward", 2: "lambda", 3: "backward", 4: "finalize", 5: "fused",
-          6: "dense", 7: "dense_backward"}
+          6: "dense", 7: "dense_backward", 8: "exchange", 9: "fused_last"}
 
 
 class tcx_shard_step(ctypes.Structure):
@@ -105,6 +105,14 @@ _sig = {
     "tcx_shard_buffers": [_vp, _vp, _i64, _i32, _vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
                           ctypes.POINTER(_i64)],
     "tcx_profile_read": [ctypes.POINTER(tcx_kernel_time), _i32, ctypes.POINTER(_i32)],
+    "tcx_comm_unique_id": [_vp],
+    "tcx_comm_init": [_vp, _i32, _i32, ctypes.POINTER(_vp)],
+    "tcx_comm_init_virtual": [_i32, ctypes.POINTER(_vp)],
+    "tcx_comm_init_host": [_i32, _i32, _vp, _vp, ctypes.POINTER(_vp)],
+    "tcx_comm_info": [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32)],
+    "tcx_sharded_workspace_bytes": [_vp, _vp, _vp, _i64, _i32, ctypes.POINTER(_sz)],
+    "tcx_grad_sharded": [_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp],
+    "tcx_expect_sharded": [_vp, _vp, _vp, _vp, _i64, _vp, _vp, _sz, _vp],
 }
 for _name, _args in _sig.items():
     f = getattr(_lib, _name)
@@ -114,10 +122,16 @@ _lib.tcx_circuit_free.argtypes = [_vp]
 _lib.tcx_circuit_free.restype = None
 _lib.tcx_pauli_free.argtypes = [_vp]
 _lib.tcx_pauli_free.restype = None
+_lib.tcx_comm_free.argtypes = [_vp]
+_lib.tcx_comm_free.restype = None
 _lib.tcx_last_error.restype = ctypes.c_char_p
 _lib.tcx_version.restype = ctypes.c_char_p
 
-EXPORTS = list(_sig) + ["tcx_circuit_free", "tcx_pauli_free", "tcx_last_error", "tcx_version"]
+EXPORTS = list(_sig) + ["tcx_circuit_free", "tcx_pauli_free", "tcx_comm_free", "tcx_last_error",
+                       "tcx_version"]
+COMM_VIRTUAL, COMM_NCCL, COMM_HOST = 0, 1, 2
+# tcx_host_exchange_fn: (user, peer, send_host, recv_host, bytes) -> 0 on success
+HOST_EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int32, _vp, ctypes.c_int32, _vp, _vp, ctypes.c_size_t)
 
 
 def _check(rc):
@@ -238,23 +252,42 @@ def _torch():
 
 
 class Workspace:
-    """Caches one device workspace per (circuit, pauli, B, mode)."""
+    """Caches one device workspace per (circuit, pauli, B, mode, device, stream).
+
+    The stream is part of the key, so calls on different streams never share scratch memory;
+    a buffer used on a stream other than the one it was allocated on is recorded on that
+    stream (record_stream), so the caching allocator does not hand it out again while kernels
+    queued there may still touch it."""
 
     def __init__(self):
         self._buf = {}
 
-    def get(self, circ, pauli, B, mode, device):
+    def get(self, circ, pauli, B, mode, device, stream=None):
         torch = _torch()
-        key = (id(circ), id(pauli) if pauli else 0, B, mode, str(device))
+        s = stream if stream is not None else torch.cuda.current_stream(device)
+        key = (id(circ), id(pauli) if pauli else 0, B, mode, str(device), s.cuda_stream)
         need = circ.workspace_bytes(pauli, B, mode)
         buf = self._buf.get(key)
         if buf is None or buf.numel() < need:
-            buf = torch.empty(max(need, 16), dtype=torch.uint8, device=device)
+            with torch.cuda.stream(s):  # allocated on the stream that uses it
+                buf = torch.empty(max(need, 16), dtype=torch.uint8, device=device)
             self._buf[key] = buf
         return buf, need
 
     def clear(self):
         self._buf.clear()
+
+
+def _on_stream(stream, *tensors):
+    """Outputs allocated on torch's current stream but written on `stream`: record them there."""
+    torch = _torch()
+    if stream is None:
+        return
+    cur = torch.cuda.current_stream(tensors[0].device) if tensors else None
+    if cur is not None and cur.cuda_stream != stream.cuda_stream:
+        for t in tensors:
+            if t is not None:
+                t.record_stream(stream)
 
 
 _default_ws = Workspace()
@@ -286,17 +319,18 @@ def expect_batch(circ: Circuit, pauli: Pauli, theta, stream=None, ws: Workspace 
     E = torch.empty(B, dtype=torch.float64, device=theta.device)
     if psi0 is not None:
         psi0 = _inputs(circ, psi0, B, theta.device)
-        buf, need = (ws or _default_ws).get(circ, pauli, B, WS_INPUTS, theta.device)
+        buf, need = (ws or _default_ws).get(circ, pauli, B, WS_INPUTS, theta.device, stream)
         _check(_lib.tcx_expect_batch_in(circ.h, pauli.h, ctypes.c_void_p(theta.data_ptr()), B,
                                         ctypes.c_void_p(psi0.data_ptr()),
                                         ctypes.c_void_p(E.data_ptr()),
                                         ctypes.c_void_p(buf.data_ptr()), buf.numel(),
                                         _stream_ptr(stream)))
         return E
-    buf, need = (ws or _default_ws).get(circ, pauli, B, 0, theta.device)
+    buf, need = (ws or _default_ws).get(circ, pauli, B, 0, theta.device, stream)
     _check(_lib.tcx_expect_batch(circ.h, pauli.h, ctypes.c_void_p(theta.data_ptr()), B,
                                  ctypes.c_void_p(E.data_ptr()), ctypes.c_void_p(buf.data_ptr()),
                                  buf.numel(), _stream_ptr(stream)))
+    _on_stream(stream, E)
     return E
 
 
@@ -315,18 +349,19 @@ def grad_batch(circ: Circuit, pauli: Pauli, theta, stream=None, ws: Workspace = 
         E, G = out
     if psi0 is not None:
         psi0 = _inputs(circ, psi0, B, theta.device)
-        buf, need = (ws or _default_ws).get(circ, pauli, B, WS_GRAD | WS_INPUTS, theta.device)
+        buf, need = (ws or _default_ws).get(circ, pauli, B, WS_GRAD | WS_INPUTS, theta.device, stream)
         _check(_lib.tcx_grad_batch_in(circ.h, pauli.h, ctypes.c_void_p(theta.data_ptr()), B,
                                       ctypes.c_void_p(psi0.data_ptr()),
                                       ctypes.c_void_p(E.data_ptr()), ctypes.c_void_p(G.data_ptr()),
                                       ctypes.c_void_p(buf.data_ptr()), buf.numel(),
                                       _stream_ptr(stream)))
         return E, G[:, :circ.P]
-    buf, need = (ws or _default_ws).get(circ, pauli, B, WS_GRAD, theta.device)
+    buf, need = (ws or _default_ws).get(circ, pauli, B, WS_GRAD, theta.device, stream)
     _check(_lib.tcx_grad_batch(circ.h, pauli.h, ctypes.c_void_p(theta.data_ptr()), B,
                                ctypes.c_void_p(E.data_ptr()), ctypes.c_void_p(G.data_ptr()),
                                ctypes.c_void_p(buf.data_ptr()), buf.numel(),
                                _stream_ptr(stream)))
+    _on_stream(stream, E, G)
     return E, G[:, :circ.P]
 
 
@@ -340,17 +375,18 @@ def state_batch(circ: Circuit, theta, stream=None, ws: Workspace = None, psi0=No
     out = torch.empty(B, 1 << circ.n, dtype=cd, device=theta.device)
     if psi0 is not None:
         psi0 = _inputs(circ, psi0, B, theta.device)
-        buf, need = (ws or _default_ws).get(circ, None, B, WS_STATE | WS_INPUTS, theta.device)
+        buf, need = (ws or _default_ws).get(circ, None, B, WS_STATE | WS_INPUTS, theta.device, stream)
         _check(_lib.tcx_state_batch_in(circ.h, ctypes.c_void_p(theta.data_ptr()), B,
                                        ctypes.c_void_p(psi0.data_ptr()),
                                        ctypes.c_void_p(out.data_ptr()),
                                        ctypes.c_void_p(buf.data_ptr()), buf.numel(),
                                        _stream_ptr(stream)))
         return out
-    buf, need = (ws or _default_ws).get(circ, None, B, WS_STATE, theta.device)
+    buf, need = (ws or _default_ws).get(circ, None, B, WS_STATE, theta.device, stream)
     _check(_lib.tcx_state_batch(circ.h, ctypes.c_void_p(theta.data_ptr()), B,
                                 ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(buf.data_ptr()),
                                 buf.numel(), _stream_ptr(stream)))
+    _on_stream(stream, out)
     return out
 
 
@@ -364,7 +400,7 @@ def grad_batch_q(circ: Circuit, pauli: Pauli, theta, stream=None, ws: Workspace 
     E = torch.empty(B, dtype=torch.float64, device=theta.device)
     G = torch.empty(B, max(circ.P, 1), dtype=torch.float64, device=theta.device)
     Q = torch.empty(B, max(circ.P, 1), dtype=torch.float64, device=theta.device)
-    buf, need = (ws or _default_ws).get(circ, pauli, B, WS_GRAD, theta.device)
+    buf, need = (ws or _default_ws).get(circ, pauli, B, WS_GRAD, theta.device, stream)
     _check(_lib.tcx_grad_batch_q(circ.h, pauli.h, ctypes.c_void_p(theta.data_ptr()), B,
                                  ctypes.c_void_p(E.data_ptr()), ctypes.c_void_p(G.data_ptr()),
                                  ctypes.c_void_p(Q.data_ptr()), ctypes.c_void_p(buf.data_ptr()),
@@ -387,7 +423,7 @@ def expect_terms_batch(circ: Circuit, pauli: Pauli, theta, stream=None, ws: Work
     if psi0 is not None:
         p0 = _inputs(circ, psi0, B, theta.device)
         mode |= WS_INPUTS
-    buf, need = (ws or _default_ws).get(circ, pauli, B, mode, theta.device)
+    buf, need = (ws or _default_ws).get(circ, pauli, B, mode, theta.device, stream)
     _check(_lib.tcx_expect_terms_batch(circ.h, pauli.h, ctypes.c_void_p(theta.data_ptr()), B,
                                        ctypes.c_void_p(p0.data_ptr()) if p0 is not None else None,
                                        ctypes.c_void_p(out.data_ptr()),
@@ -407,7 +443,7 @@ def grad_batch_host(circ: Circuit, pauli: Pauli, theta_host: np.ndarray, E_host=
     if grad_host is None:
         grad_host = np.empty((B, max(circ.P, 1)), dtype=np.float64)
     dev = device or torch.device("cuda", torch.cuda.current_device())
-    buf, need = (ws or _default_ws).get(circ, pauli, B, WS_GRAD | WS_HOST_IO, dev)
+    buf, need = (ws or _default_ws).get(circ, pauli, B, WS_GRAD | WS_HOST_IO, dev, stream)
     _check(_lib.tcx_grad_batch_host(circ.h, pauli.h, ctypes.c_void_p(theta_host.ctypes.data), B,
                                     ctypes.c_void_p(E_host.ctypes.data),
                                     ctypes.c_void_p(grad_host.ctypes.data),
@@ -438,10 +474,134 @@ def expect_batch_host(circ: Circuit, pauli: Pauli, theta_host: np.ndarray, E_hos
     if E_host is None:
         E_host = np.empty(B, dtype=np.float64)
     dev = device or torch.device("cuda", torch.cuda.current_device())
-    buf, need = (ws or _default_ws).get(circ, pauli, B, WS_HOST_IO, dev)
+    buf, need = (ws or _default_ws).get(circ, pauli, B, WS_HOST_IO, dev, stream)
     th = theta_host if theta_host.size else np.zeros((B, 1))
     _check(_lib.tcx_expect_batch_host(circ.h, pauli.h, ctypes.c_void_p(th.ctypes.data), B,
                                       ctypes.c_void_p(E_host.ctypes.data),
                                       ctypes.c_void_p(buf.data_ptr()), buf.numel(),
                                       _stream_ptr(stream)))
     return E_host
+
+
+# ------------------------------------------------------------ sharded state
+class Comm:
+    """tcx_comm handle (include/tcx.h): the library owns the exchange of a sharded state.
+
+    Comm.virtual(G)      all G ranks in this process on the current device;
+    Comm.nccl(group)     one process per GPU; the ncclUniqueId is made by the library on
+                         rank 0 and broadcast with torch.distributed (plumbing only);
+    Comm.host(group)     several processes on one device, exchanges staged through host
+                         memory and a torch.distributed (gloo) send/recv callback (tests).
+    """
+
+    def __init__(self, h, keep=None):
+        self.h = h
+        self._keep = keep  # the ctypes callback must outlive the handle
+        kind, world, rank = _i32(), _i32(), _i32()
+        _check(_lib.tcx_comm_info(h, ctypes.byref(kind), ctypes.byref(world), ctypes.byref(rank)))
+        self.kind, self.world, self.rank = kind.value, world.value, rank.value
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.tcx_comm_free(self.h)
+            self.h = None
+
+    @classmethod
+    def virtual(cls, world: int) -> "Comm":
+        h = _vp()
+        _check(_lib.tcx_comm_init_virtual(world, ctypes.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def nccl(cls, group=None) -> "Comm":
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        uid = (ctypes.c_char * 128)()
+        if rank == 0:
+            _check(_lib.tcx_comm_unique_id(uid))
+        obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group else 0,
+                                   group=group)
+        uid = (ctypes.c_char * 128).from_buffer_copy(obj[0])
+        h = _vp()
+        _check(_lib.tcx_comm_init(uid, world, rank, ctypes.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def host(cls, group=None) -> "Comm":
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        fn = HOST_EXCHANGE_FN(host_exchange_callback(group))
+        h = _vp()
+        _check(_lib.tcx_comm_init_host(world, rank, fn, None, ctypes.byref(h)))
+        return cls(h, keep=fn)
+
+
+def host_exchange_callback(group=None):
+    """The host transport's send/recv: `bytes` host bytes to and from rank `peer` over a
+    torch.distributed (gloo) group; returns a Python callable of the tcx_host_exchange_fn
+    signature (wrap it in HOST_EXCHANGE_FN)."""
+    import torch
+    import torch.distributed as dist
+
+    def fn(user, peer, send_ptr, recv_ptr, nbytes):
+        try:
+            if not 0 <= peer < dist.get_world_size(group) or peer == dist.get_rank(group):
+                raise ValueError(f"peer {peer} is not another rank of the group")
+            gpeer = dist.get_global_rank(group, peer) if group is not None else peer
+            sb = (ctypes.c_uint8 * nbytes).from_address(send_ptr)
+            rb = (ctypes.c_uint8 * nbytes).from_address(recv_ptr)
+            st = torch.frombuffer(sb, dtype=torch.uint8)
+            rt = torch.frombuffer(rb, dtype=torch.uint8)
+            reqs = dist.batch_isend_irecv([dist.P2POp(dist.isend, st, gpeer, group),
+                                           dist.P2POp(dist.irecv, rt, gpeer, group)])
+            for r in reqs:
+                r.wait()
+            return 0
+        except Exception as ex:  # reported as TCX_E_NCCL by the library
+            import sys
+            print(f"tcx host exchange failed: {ex!r}", file=sys.stderr)
+            return 1
+    return fn
+
+
+def sharded_workspace_bytes(circ: Circuit, pauli: Pauli, comm: Comm, B: int, grad: bool) -> int:
+    out = _sz()
+    _check(_lib.tcx_sharded_workspace_bytes(circ.h, pauli.h, comm.h, B, int(grad),
+                                            ctypes.byref(out)))
+    return out.value
+
+
+def grad_sharded(circ: Circuit, pauli: Pauli, comm: Comm, theta, ws=None, stream=None, out=None):
+    """(E [B], grad [B, P]) of a state sharded over comm.world ranks (tcx_grad_sharded): the
+    library runs every pass, exchange and the final sum over ranks."""
+    torch = _torch()
+    theta = theta.contiguous()
+    assert theta.dtype == torch.float64 and theta.is_cuda
+    B = theta.shape[0]
+    if out is None:
+        E = torch.empty(B, dtype=torch.float64, device=theta.device)
+        G = torch.empty(B, max(circ.P, 1), dtype=torch.float64, device=theta.device)
+    else:
+        E, G = out
+    need = sharded_workspace_bytes(circ, pauli, comm, B, True)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(max(need, 16), dtype=torch.uint8, device=theta.device)
+    _check(_lib.tcx_grad_sharded(circ.h, pauli.h, comm.h, ctypes.c_void_p(theta.data_ptr()), B,
+                                 ctypes.c_void_p(E.data_ptr()), ctypes.c_void_p(G.data_ptr()),
+                                 ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream)))
+    return E, G[:, :circ.P]
+
+
+def expect_sharded(circ: Circuit, pauli: Pauli, comm: Comm, theta, ws=None, stream=None):
+    torch = _torch()
+    theta = theta.contiguous()
+    B = theta.shape[0]
+    E = torch.empty(B, dtype=torch.float64, device=theta.device)
+    need = sharded_workspace_bytes(circ, pauli, comm, B, False)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(max(need, 16), dtype=torch.uint8, device=theta.device)
+    _check(_lib.tcx_expect_sharded(circ.h, pauli.h, comm.h, ctypes.c_void_p(theta.data_ptr()), B,
+                                   ctypes.c_void_p(E.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
+                                   ws.numel(), _stream_ptr(stream)))
+    return E

@@ -38,5 +38,18 @@ def check_grad(G_gpu, G_ref, H, circ, dtype, what=""):
     return err.max()
 
 
-def state_tol(dtype, n_gates):
-    return (2e-6 * np.sqrt(max(n_gates, 1)) + 1e-6) if dtype == "c64" else 1e-12 * max(n_gates, 1)
+EPS = {"c64": 2.0 ** -24, "c128": 2.0 ** -53}
+
+
+def check_state(psi_gpu, psi_ref, dtype, n_gates, what=""):
+    """State parity relative to the arithmetic's precision: each of the n_gates gate
+    applications rounds every amplitude at a few eps (unit roundoff of the state dtype,
+    including the rounding of its matrix entries), and independent roundings add in
+    quadrature, so ||psi_gpu - psi_ref||_2 <= 32 eps sqrt(G) ||psi_ref||_2 (normwise; it
+    bounds every amplitude's error too).  Returns the normwise relative error."""
+    d = np.asarray(psi_gpu).reshape(-1) - np.asarray(psi_ref).reshape(-1)
+    nr = max(float(np.linalg.norm(np.asarray(psi_ref).reshape(-1))), 1e-300)
+    rel = float(np.linalg.norm(d)) / nr
+    tol = 32.0 * EPS[dtype] * np.sqrt(max(n_gates, 1))
+    assert rel <= tol, f"{what} state normwise rel err {rel:.3e} > {tol:.3e} (G={n_gates})"
+    return rel

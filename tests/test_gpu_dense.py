@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 import workloads as W
-from helpers import check_E, check_grad, state_tol
+from helpers import check_E, check_grad, check_state
 from oracle import oracle as orc
 
 pytestmark = pytest.mark.gpu
@@ -39,8 +39,7 @@ def test_dense_state_random_all_kinds(tc, dtype, k, n):
     psi = tc.state_batch(C, _th(th)).cpu().numpy()
     for b in range(3):
         ref = orc.state(c, th[b])
-        err = np.abs(psi[b] - ref).max()
-        assert err <= state_tol(dtype, len(c.gates)), f"k={k} row {b}: {err}"
+        check_state(psi[b], ref, dtype, len(c.gates), f"k={k} row {b}")
 
 
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
@@ -100,7 +99,7 @@ def test_dense_random_deep_matches_window_path(tc, k):
     C = tc.Circuit(c, "c128", dense_k=k)
     psi = tc.state_batch(C, _th(np.zeros((1, 0)))).cpu().numpy()[0]
     ref = orc.state(c, np.zeros(0))
-    assert np.abs(psi - ref).max() <= state_tol("c128", len(c.gates))
+    check_state(psi, ref, "c128", len(c.gates))
 
 
 def test_dense_roundtrip_u_udagger_30q(tc):
@@ -132,7 +131,7 @@ def test_dense_k5_c64_tensor_core_multi_tile(tc, n, B):
     psi = tc.state_batch(C, _th(np.zeros((B, 0)))).cpu().numpy()
     ref = orc.state(c, np.zeros(0))
     for b in range(B):
-        assert np.abs(psi[b] - ref).max() <= state_tol("c64", len(c.gates))
+        check_state(psi[b], ref, "c64", len(c.gates))
 
 
 @pytest.mark.parametrize("low", [True, False])
@@ -156,7 +155,7 @@ def test_dense_k5_c64_tensor_core_pair_modes(tc, low):
     psi = tc.state_batch(C, _th(np.zeros((2, 0)))).cpu().numpy()
     ref = orc.state(c, np.zeros(0))
     for b in range(2):
-        assert np.abs(psi[b] - ref).max() <= state_tol("c64", len(c.gates))
+        check_state(psi[b], ref, "c64", len(c.gates))
 
 
 @pytest.mark.parametrize("dtype", ["c64", "c128"])

@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 import workloads as W
-from helpers import check_E, check_grad, state_tol
+from helpers import check_E, check_grad, check_state
 from oracle import oracle as orc
 
 pytestmark = pytest.mark.gpu
@@ -68,7 +68,7 @@ def test_fuzz_parity(tc, seed):
     P = tc.Pauli(H)
     psi = tc.state_batch(C, _th(th)).cpu().numpy()
     for b in range(th.shape[0]):
-        assert np.abs(psi[b] - orc.state(c, th[b])).max() <= state_tol(dtype, len(c.gates)), (seed, opts)
+        check_state(psi[b], orc.state(c, th[b]), dtype, len(c.gates))
     E, G = tc.grad_batch(C, P, _th(th))
     Er, Gr = orc.value_grad_batch(c, H, th, nthreads=os.cpu_count() or 1)
     check_E(E.cpu().numpy(), Er, H, dtype, f"seed {seed} {opts}")

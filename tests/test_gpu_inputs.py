@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 import workloads as W
-from helpers import check_E, check_grad, state_tol
+from helpers import check_E, check_grad, check_state
 from oracle import oracle as orc
 
 pytestmark = pytest.mark.gpu
@@ -52,7 +52,7 @@ def test_inputs_state_and_grad(tc, dtype, opt):
     psi = tc.state_batch(C, _th(th), psi0=_dev(p0, dtype)).cpu().numpy()
     for b in range(B):
         ref = orc.state_in(c, th[b], p0[b])
-        assert np.abs(psi[b] - ref).max() <= state_tol(dtype, len(c.gates))
+        check_state(psi[b], ref, dtype, len(c.gates))
     E, G = tc.grad_batch(C, P, _th(th), psi0=_dev(p0, dtype))
     Er, Gr = orc.value_grad_batch_in(c, H, th, p0, nthreads=os.cpu_count() or 1)
     check_E(E.cpu().numpy(), Er, H, dtype)

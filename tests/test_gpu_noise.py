@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 import workloads as W
-from helpers import check_E, check_grad, state_tol
+from helpers import check_E, check_grad, check_state
 from oracle import oracle as orc
 
 pytestmark = pytest.mark.gpu
@@ -42,7 +42,7 @@ def test_noisy_vqe_trajectories(tc, dtype, opts):
     assert np.all(G.cpu().numpy()[:, 3 * n * d:] == 0.0)
     psi = tc.state_batch(C, _th(th)).cpu().numpy()
     for b in range(2):
-        assert np.abs(psi[b] - orc.state(c, th[b])).max() <= state_tol(dtype, len(c.gates))
+        check_state(psi[b], orc.state(c, th[b]), dtype, len(c.gates))
 
 
 def test_trajectory_average_matches_channel(tc):

@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import workloads as W
-from helpers import check_E, check_grad, state_tol
+from helpers import check_E, check_grad, check_state
 from oracle import oracle as orc
 
 pytestmark = pytest.mark.gpu
@@ -52,8 +52,7 @@ def test_state_random_all_kinds_single_tile(tc, dtype, n, jit):
     psi = tc.state_batch(C, _th(th)).cpu().numpy()
     for b in range(3):
         ref = orc.state(c, th[b])
-        err = np.abs(psi[b] - ref).max()
-        assert err <= state_tol(dtype, len(c.gates)), f"row {b}: {err}"
+        check_state(psi[b], ref, dtype, len(c.gates), f"row {b}")
 
 
 @pytest.mark.parametrize("jit", [True, False])
@@ -69,7 +68,7 @@ def test_state_multi_pass(tc, dtype, n, t, jit):
     psi = tc.state_batch(C, _th(th)).cpu().numpy()
     for b in range(2):
         ref = orc.state(c, th[b])
-        assert np.abs(psi[b] - ref).max() <= state_tol(dtype, len(c.gates))
+        check_state(psi[b], ref, dtype, len(c.gates))
 
 
 def test_fig2_golden_on_gpu(tc):

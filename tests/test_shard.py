@@ -1,7 +1,10 @@
 """Sharded single state (north_star: top log2(G) global qubits + all-to-all qubit swaps).
 
-CPU: the exchange's data movement with world_size-2 gloo all-to-all, and the plan's
-exchange points.  GPU: G virtual ranks in one process (device-copy exchanges) vs the oracle.
+CPU: the host transport's gloo send/recv callback at world size 2, the program's structure and
+the layout search's exchange counts.  GPU (all through tcx_grad_sharded, the library-owned
+exchange): G virtual ranks in one process (in-place swap kernels) vs the oracle and closed
+forms; two processes sharing cuda:0 with the host-staged gloo transport vs the oracle; the NCCL
+communicator at world size 1 (one GPU in this run).
 """
 import os
 import socket
@@ -22,51 +25,53 @@ def _free_port():
     return p
 
 
-def _reference_exchange(bufs):
-    """rank r's block k <- rank k's block r (plain loops)."""
-    G = len(bufs)
-    out = [b.clone() for b in bufs]
-    for r in range(G):
-        for k in range(G):
-            out[r][:, k, :] = bufs[k][:, r, :]
-    return out
-
-
-def test_exchange_virtual_matches_definition():
-    from paper_2205_10091_b200.shard import exchange_virtual
-    g = torch.Generator().manual_seed(0)
-    for G, B, C in [(2, 1, 8), (4, 3, 5), (8, 2, 4)]:
-        bufs = [torch.randn(B, G, C, generator=g, dtype=torch.float64) for _ in range(G)]
-        want = _reference_exchange(bufs)
-        exchange_virtual(bufs)
-        for r in range(G):
-            assert torch.equal(bufs[r], want[r])
-
-
-def _worker(rank, world, port, data, out, chunk):
+def _cb_worker(rank, world, port, out):
+    """Two CPU processes exchange host buffers through the library's host-transport callback
+    (tcx.host_exchange_callback: gloo isend/irecv), as tcx_grad_sharded calls it."""
+    import ctypes
     import torch.distributed as dist
-    from paper_2205_10091_b200.shard import exchange_dist
+    from paper_2205_10091_b200 import tcx
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    buf = data[rank].clone()
-    exchange_dist(buf, max_chunk_bytes=chunk)
-    out[rank] = buf.numpy().copy()
+    fn = tcx.HOST_EXCHANGE_FN(tcx.host_exchange_callback())
+    for nbytes in (8, 4096, 3 << 20):
+        send = (ctypes.c_uint8 * nbytes)()
+        ctypes.memset(send, 17 + rank, nbytes)
+        recv = (ctypes.c_uint8 * nbytes)()
+        rc = fn(None, 1 - rank, ctypes.addressof(send), ctypes.addressof(recv), nbytes)
+        out[(rank, nbytes)] = (rc, bytes(recv[:4]), bytes(recv[-4:]))
+    # a failing transfer reports non-zero (the library turns it into TCX_E_NCCL)
+    out[(rank, "bad")] = fn(None, 5, ctypes.addressof(send), ctypes.addressof(recv), 8)
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("chunk", [1 << 30, 64])
-def test_exchange_dist_gloo_world2(chunk):
-    """The NCCL-path exchange (torch all_to_all_single, sub-chunk staging) on gloo."""
-    G, B, C = 2, 3, 16
-    g = torch.Generator().manual_seed(1)
-    data = [torch.randn(B, G, C, generator=g, dtype=torch.float64) for _ in range(G)]
-    want = _reference_exchange(data)
+def test_host_exchange_callback_gloo_world2():
     manager = mp.Manager()
     out = manager.dict()
-    mp.spawn(_worker, args=(G, _free_port(), data, out, chunk), nprocs=G, join=True)
-    for r in range(G):
-        np.testing.assert_array_equal(out[r], want[r].numpy())
+    mp.spawn(_cb_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    for r in range(2):
+        for nbytes in (8, 4096, 3 << 20):
+            rc, head, tail = out[(r, nbytes)]
+            assert rc == 0 and head == bytes([17 + (1 - r)] * 4) and tail == head
+        assert out[(r, "bad")] != 0
+
+
+def test_sharded_layout_search_cfg5():
+    """cfg5's 36-qubit / 8-rank plan (and 34 / 35 on 2 / 4 ranks): the layout search puts the far
+    end of the CNOT ladder in the top local bits, so the light cone sweeps a band of layers per
+    segment: 3 layouts, 2 psi exchanges forward, 4 psi+lambda (2 backward, 2 around the
+    lambda units flipping global qubits) -- round 1's fixed layout needed 9 layouts and
+    8 + 10 exchanges."""
+    from paper_2205_10091_b200 import tcx
+    from paper_2205_10091_b200.shard import exchange_counts
+    for n, g in ((34, 1), (35, 2), (36, 3)):
+        name, c, H, th, dt = W.config(4, n=n)
+        C, P = tcx.Circuit(c, "c64", global_bits=g), tcx.Pauli(H)
+        info = C.info(P)
+        assert info["segments"] == 3 and info["fwd_passes"] <= 12, info
+        assert exchange_counts(C, P) == (2, 4)
+        assert exchange_counts(C, P, want_grad=False)[1] == 0
 
 
 def test_shard_program_structure():
@@ -134,3 +139,65 @@ def test_sharded_ghz_ry_closed_form_virtual():
     nb[:, 1:] += ct[:, :-1]
     nb[:, :-1] += ct[:, 1:]
     np.testing.assert_allclose(G.cpu().numpy(), -st * nb, atol=1e-5 * H.l1)
+
+
+def _host_worker(rank, world, port, out, n, d, g, dtype):
+    import torch.distributed as dist
+    from paper_2205_10091_b200 import tcx
+    from paper_2205_10091_b200.shard import ShardedState
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    c, H = W.hea(n, d), W.tfim_zz_x(n)
+    th = W.thetas(2, c.n_params, 77)
+    S = ShardedState(c, H, dtype, g, comm=tcx.Comm.host(), tile_bits=8)
+    E, G = S.run(torch.as_tensor(th).cuda())
+    E2, _ = S.run(torch.as_tensor(th).cuda(), want_grad=False)
+    out[rank] = (E.cpu().numpy(), G.cpu().numpy(), E2.cpu().numpy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,d,dtype", [(13, 3, "c64"), (12, 2, "c128")])
+def test_sharded_host_transport_two_processes(n, d, dtype):
+    """World size 2 as two processes on cuda:0: every exchange and the final sum go through
+    the library's host transport (gloo) -- the same tcx_grad_sharded entry and program as the
+    NCCL path, one process per rank.  Both ranks return the full E and gradient."""
+    from helpers import check_E, check_grad
+    from oracle import oracle as orc
+    manager = mp.Manager()
+    out = manager.dict()
+    mp.spawn(_host_worker, args=(2, _free_port(), out, n, d, 1, dtype), nprocs=2, join=True)
+    c, H = W.hea(n, d), W.tfim_zz_x(n)
+    th = W.thetas(2, c.n_params, 77)
+    Er, Gr = orc.value_grad_batch(c, H, th)
+    for r in range(2):
+        E, G, E2 = out[r]
+        check_E(E, Er, H, dtype, f"rank {r} E")
+        check_grad(G, Gr, H, c, dtype, f"rank {r} grad")
+        check_E(E2, Er, H, dtype, f"rank {r} expect")
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+
+
+@pytest.mark.gpu
+def test_nccl_comm_world1():
+    """The NCCL communicator (tcx_comm_unique_id / tcx_comm_init, libnccl resolved at run
+    time) at world size 1 on an unsharded circuit: tcx_grad_sharded = tcx_grad_batch, with the
+    final ncclAllReduce a no-op."""
+    import ctypes
+    from paper_2205_10091_b200 import tcx
+    uid = (ctypes.c_char * 128)()
+    tcx._check(tcx._lib.tcx_comm_unique_id(uid))
+    h = tcx._vp()
+    tcx._check(tcx._lib.tcx_comm_init(uid, 1, 0, ctypes.byref(h)))
+    comm = tcx.Comm(h)
+    assert comm.kind == tcx.COMM_NCCL and comm.world == 1
+    c, H = W.hea(10, 2), W.tfim_zz_x(10)
+    th = torch.as_tensor(W.thetas(3, c.n_params, 4)).cuda()
+    C, P = tcx.Circuit(c, "c64"), tcx.Pauli(H)
+    E, G = tcx.grad_sharded(C, P, comm, th)
+    E0, G0 = tcx.grad_batch(C, P, th)
+    assert torch.equal(E, E0) and torch.equal(G, G0)
+    with pytest.raises(tcx.TcxError):  # world 1 cannot run a 2-rank plan
+        tcx.grad_sharded(tcx.Circuit(c, "c64", global_bits=1), P, comm, th)
