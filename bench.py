@@ -191,6 +191,10 @@ def main():
     ap.add_argument("--config", type=int, default=1,
                     help="BASELINE.json configs index (5: the paper's Table VII barren-plateau task)")
     ap.add_argument("--batch", type=int, default=None, help="theta rows per rank")
+    ap.add_argument("--qubits", type=int, default=None,
+                    help="override the config's qubit count (e.g. config 1 at n = 14..17 with --cluster-bits)")
+    ap.add_argument("--cluster-bits", type=int, default=0,
+                    help="cluster-resident states (SURVEY §8f f1): 2^g CTAs per theta row")
     ap.add_argument("--batch-qubits", type=int, default=None,
                     help="config 4: local qubits per rank (default 33)")
     ap.add_argument("--tile-bits", type=int, default=0)
@@ -237,7 +241,9 @@ def main():
     if args.config == 4 and (world > 1 or args.virtual_ranks > 1):
         return run_sharded(args, world, rank, local, dev)
 
-    name, circ, H, theta, dtype = W.config(args.config, B=args.batch)
+    name, circ, H, theta, dtype = W.config(args.config, B=args.batch, n=args.qubits)
+    if args.qubits:
+        name = name.replace(f"{W.config(args.config, B=1)[1].n}_", f"{args.qubits}_", 1)
     if args.dtype and args.dtype != dtype:
         name, dtype = name.replace("_" + dtype, "_" + args.dtype), args.dtype
     B = theta.shape[0]
@@ -247,7 +253,8 @@ def main():
     C = tcx.Circuit(circ, dtype, tile_bits=args.tile_bits, coalesce_bits=args.coalesce_bits,
                     reg_bits=args.reg_bits,
                     max_ops_per_pass=args.max_ops_per_pass,
-                    jit=bool(args.jit), dense_k=args.dense_k, l2_rows=args.l2_rows)
+                    jit=bool(args.jit), dense_k=args.dense_k, l2_rows=args.l2_rows,
+                    cluster_bits=args.cluster_bits)
     P = tcx.Pauli(H)
     t_jit = time.perf_counter()
     mode = args.mode or ("expect" if circ.n_params == 0 else "grad")
@@ -399,7 +406,8 @@ def main():
                     "frac": ach / (hbm_peak / 1e9)}
         jitk = {"forward": "tcx_jit_fwd_*", "backward": "tcx_jit_bwd_*", "lambda": "tcx_jit_lam_*",
                 "fused": "tcx_jit_mega_*", "fused_last": "tcx_jit_mega_* (last pass)"}
-        kname = {"dense": "dense_fwd_kernel / dense_fwd_tc_kernel (dense k-qubit blocks)",
+        kname = {"cluster": "tcx_jit_cluster_* (cluster-resident megakernel, whole program)",
+                 "dense": "dense_fwd_kernel / dense_fwd_tc_kernel (dense k-qubit blocks)",
                  "dense_backward": "dense_bwd_kernel (dense k-qubit blocks, adjoint)"}.get(
                      dom, (f"{jitk.get(dom, dom)} (per-circuit JIT window passes, {dom})"
                            if info.get("jit") else f"pass_kernel ({dom} passes)"))
@@ -436,7 +444,7 @@ def main():
                                                  "n_ops", "jit", "dense_k", "dense_blocks")},
                    "jit_compile_s": round(t_jit, 2), "mode": mode,
                    "max_ops_per_pass": args.max_ops_per_pass, "dense_k": args.dense_k,
-                   "l2_rows": args.l2_rows,
+                   "l2_rows": args.l2_rows, "cluster_bits": args.cluster_bits,
                    "launch": graph_note + ("; per-kernel times from one extra eager profiled step"
                                            if used_graph else
                                            "; per-kernel CUDA events inside the timed region")},

@@ -121,6 +121,14 @@ typedef struct {
                                groups of this many theta rows in turn, so a group's psi and
                                lambda stay in L2 between passes; -1 = auto (groups whose psi +
                                lambda fit ~96 MB); 0 = off (every pass over all rows) */
+    int32_t cluster_bits;   /* cluster-resident states: g_c in [1, 4] runs each
+                               theta row on one thread-block cluster of 2^g_c CTAs (one per SM)
+                               whose REGISTERS hold the whole psi and lambda (2^(n-g_c)
+                               amplitudes per CTA, at most 2^13 complex64 / 2^12 complex128);
+                               gates on the top g_c qubits trade places through distributed
+                               shared memory, so HBM carries only theta in and E / grad out;
+                               one launch per batch.  tcx_expect_batch / tcx_grad_batch only;
+                               0 = off */
 } tcx_build_opts;
 
 /* Executed-plan summary (for reports and tests). */
@@ -143,6 +151,7 @@ typedef struct {
     int32_t dense_k;          /* dense block size cap (0: no dense blocks) */
     int32_t dense_blocks;     /* dense k-qubit block passes (each one read+write of psi) */
     int32_t init_h;           /* leading H gates folded into the initial |+> state */
+    int32_t cluster_bits;     /* cluster-resident plan: CTAs per theta row = 2^cluster_bits */
 } tcx_plan_info;
 
 typedef struct tcx_circuit tcx_circuit;
@@ -357,7 +366,8 @@ typedef struct {
                         4 finalize, 5 fused single pass (forward + lambda + backward),
                         6 dense block, 7 dense block backward, 8 sharded-state exchange
                         (bytes = data that changes rank; virtual ranks: HBM read + write),
-                        9 last forward pass fused with lambda and its backward */
+                        9 last forward pass fused with lambda and its backward,
+                        10 cluster-resident megakernel (whole program; bytes = HBM in/out) */
     int32_t index;   /* pass / lambda-unit index */
     float ms;
     float pad;

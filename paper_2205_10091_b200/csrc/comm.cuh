@@ -311,6 +311,7 @@ tcx_status run_sharded(Plan& P, const tcx_pauli* H, tcx_comm* c, const double* t
   if (!H || !c) return fail(TCX_E_INVALID, "null pauli or comm");
   if (B <= 0) return fail(TCX_E_INVALID, "B must be > 0");
   if (!E || (kind == K_GRAD && P.P > 0 && !grad)) return fail(TCX_E_INVALID, "null output");
+  if (P.cluster) return fail(TCX_E_INVALID, "cluster-resident plans run on one GPU (tcx_grad_batch)");
   if (c->world != (1 << P.gbits))
     return fail(TCX_E_INVALID, "comm world size " + std::to_string(c->world) +
                                    " != 2^global_bits = " + std::to_string(1 << P.gbits));

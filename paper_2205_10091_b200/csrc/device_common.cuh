@@ -254,6 +254,23 @@ __device__ __forceinline__ void tma_store_commit_wait() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
+// thread-block clusters (cluster-resident states): this CTA's rank, a full cluster barrier
+// (release / acquire: shared-memory writes before it are visible to every CTA after it), and
+// the generic address of the same shared-memory location in another CTA of the cluster
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void* cluster_map(void* p, uint32_t rank) {
+  uint64_t r;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(r) : "l"((uint64_t)p), "r"(rank));
+  return (void*)r;
+}
+
 template <int N>
 struct IC {
   static constexpr int value = N;
@@ -579,6 +596,52 @@ __device__ __forceinline__ void op_bwd(const KOp& o, Cx<Real>* v, Cx<Real>* l,
 // (P psi)_r = i^nY (-1)^popc((r ^ x) & zy) psi_{r ^ x}; the sign of x & zy is folded into
 // the host-side coefficient.  Partners come from the shared-memory tile, or from HBM when
 // x leaves the window (KGroup::global).
+// lambda = H psi over the groups [groups, groups + count) for a tile held in registers
+// (T0 mapping), every flip mask inside the tile (cluster-resident megakernel)
+template <typename Real, int RB>
+__device__ __forceinline__ Real lambda_tile_g(const KGroup* groups, int count, const KPTerm* pterms,
+                                              Cx<Real>* v, Cx<Real>* l, const Map<RB>& top,
+                                              Cx<Real>* xp, const uint32_t* s_swb, int t) {
+  using C = Cx<Real>;
+  constexpr int NR = 1 << RB;
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < NR; ++j) xp[sidx(top, j)] = v[j];
+  __syncthreads();
+  Real e = 0;
+  for (int g = 0; g < count; ++g) {
+    const KGroup G = groups[g];
+    uint32_t swx = 0;
+    for (int p = 0; p < t; ++p)
+      if (G.xlocal >> p & 1u) swx ^= s_swb[p];
+    Real cr[NR], ci[NR];
+#pragma unroll
+    for (int j = 0; j < NR; ++j) cr[j] = ci[j] = 0;
+    for (int k = 0; k < G.term_count; ++k) {
+      const KPTerm pt = pterms[G.term_begin + k];
+      const uint32_t tp = __popcll((top.g | top.gb) & pt.zy) & 1u;
+      const uint32_t mr = regmask<RB>(top, pt.zy);
+      const Real re = (Real)pt.cre, im = (Real)pt.cim;
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        const uint32_t s = tp ^ (__popc((uint32_t)j & mr) & 1u);
+        cr[j] += s ? -re : re;
+        ci[j] += s ? -im : im;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      const C p = xp[sidx(top, j) ^ swx];
+      const Real dx = cr[j] * p.x - ci[j] * p.y;
+      const Real dy = cr[j] * p.y + ci[j] * p.x;
+      e += v[j].x * dx + v[j].y * dy;
+      l[j].x += dx;
+      l[j].y += dy;
+    }
+  }
+  return e;
+}
+
 template <typename Real, int RB>
 __device__ __forceinline__ Real lambda_tile(const PassArgs& a, Cx<Real>* v, Cx<Real>* l,
                                             const Map<RB>& top, Cx<Real>* xp,

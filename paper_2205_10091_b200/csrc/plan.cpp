@@ -857,10 +857,31 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
   }
   // ---- options
   const bool c128 = dtype == TCX_C128;
-  const int gb = opts ? std::max(0, opts->global_bits) : 0;
+  int gb = opts ? std::max(0, opts->global_bits) : 0;
   if (gb > 0 && (gb > 6 || n - gb < 2 * gb + 2)) {
     err = "global_bits must be in [1, 6] with n - g >= 2g + 2 local bits";
     return TCX_E_INVALID;
+  }
+  // Cluster-resident states: the plan of a state "sharded" over the 2^g_c
+  // CTAs of one thread-block cluster, one tile per CTA (t = n - g_c), run by one JIT
+  // megakernel per batch whose registers hold psi and lambda (jit.cpp cluster_kernel).
+  const int cb = opts ? std::max(0, opts->cluster_bits) : 0;
+  if (cb > 0) {
+    if (gb > 0) {
+      err = "cluster_bits and global_bits are exclusive";
+      return TCX_E_INVALID;
+    }
+    if (cb > 4 || n - cb < 2 * cb + 2 || n - cb > (c128 ? 12 : 13)) {
+      err = "cluster_bits must be in [1, 4] with 2 cluster_bits + 2 <= n - cluster_bits <= 13 "
+            "(complex64) / 12 (complex128)";
+      return TCX_E_INVALID;
+    }
+    if (opts && opts->dense_k > 0) {
+      err = "dense_k is not supported with cluster_bits";
+      return TCX_E_UNSUPPORTED;
+    }
+    gb = cb;
+    P.cluster = true;
   }
   P.gbits = gb;
   P.nloc = n - gb;
@@ -871,7 +892,9 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
   if (t >= n - gb) t = n - gb;
   // register bits per stage: 4 for full tiles; small single-tile states use more threads per
   // tile (latency-bound: cfg1 n=10 c128 measured 255k -> 287k circuits/s with r = 2)
+  if (P.cluster) t = n - gb;  // the whole local state is one tile
   int r = opts && opts->reg_bits > 0 ? opts->reg_bits : (t < tdef ? (n - gb <= 10 ? 2 : 3) : 4);
+  if (P.cluster) r = std::max(r, gb);  // the exchange moves register slots (top local bits)
   r = std::min(r, kMaxRegBits);
   if (r > t) r = t;
   if (t - r > 9) r = t - 9;  // at most 512 threads per tile (kernel launch bounds)
@@ -915,7 +938,7 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
   // kernels when tiles pair up and a sub-tile has whole warps
   // software-pipelined TMA tiles (prefetch of tile i+1 into its own buffer while tile i is
   // computed; the store of tile i drains while tile i+1 runs)
-  P.jit_pipe = getenv("TCX_JIT_PIPE") ? atoi(getenv("TCX_JIT_PIPE")) != 0 : false;
+  P.jit_pipe = getenv("TCX_JIT_PIPE") ? (atoi(getenv("TCX_JIT_PIPE")) != 0 ? 1 : 0) : -1;
   P.jit_nsub = 1;  // 2 = lock-stepped sub-tiles (measured slower with FFMA2 code; opt-in via TCX_JIT_NSUB)
   if (const char* e = getenv("TCX_JIT_NSUB"))
     if (atoi(e) == 2 && P.tpc % 2 == 0 && P.h >= 5) P.jit_nsub = 2;
@@ -1559,6 +1582,43 @@ std::shared_ptr<Binding> bind(Plan& P, const Pauli& H) {
     }
   }
   return B;
+}
+
+// The fixed step list of a sharded program (identical on every rank): materialise, forward
+// passes with an EXCHANGE between segments, lambda units (those flipping global qubits run
+// after an exchange), backward passes mirrored, finalise.
+std::vector<tcx_shard_step> shard_program(const Plan& P, const Binding& Bdr, bool want_grad) {
+  const Binding* Bd = &Bdr;
+  std::vector<tcx_shard_step> v;
+  auto add = [&](int k, int a) { v.push_back({k, a}); };
+  const int nP = (int)P.passes.size();
+  add(TCX_STEP_MATERIALIZE, 0);
+  for (int p = 0; p < nP; ++p) {
+    if (p > 0 && P.passes[p].seg != P.passes[p - 1].seg) add(TCX_STEP_EXCHANGE, 1);
+    add(TCX_STEP_FWD, p);
+  }
+  const int x = want_grad ? 3 : 1;  // exchange psi (+ lambda once it exists)
+  bool any_lam = false;
+  for (int u = 0; u < (int)Bd->units.size(); ++u)
+    if (!Bd->units[u].swapped) {
+      add(TCX_STEP_LAMBDA, u);
+      any_lam = true;
+    }
+  bool sw = false;
+  for (int u = 0; u < (int)Bd->units.size(); ++u)
+    if (Bd->units[u].swapped) {
+      if (!sw) add(TCX_STEP_EXCHANGE, any_lam ? x : 1);
+      sw = true;
+      add(TCX_STEP_LAMBDA, u);
+    }
+  if (sw && want_grad) add(TCX_STEP_EXCHANGE, x);  // back to the backward's layout
+  if (want_grad)
+    for (int p = nP - 1; p >= 0; --p) {
+      add(TCX_STEP_BWD, p);
+      if (p > 0 && P.passes[p].seg != P.passes[p - 1].seg) add(TCX_STEP_EXCHANGE, 3);
+    }
+  add(TCX_STEP_FINALIZE, 0);
+  return v;
 }
 
 }  // namespace tcx

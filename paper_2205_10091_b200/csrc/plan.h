@@ -192,7 +192,8 @@ struct Plan {
   int64_t tiles = 1;             // 2^(n - t)
   int tpc = 1;                   // tiles per CTA (depends on the tile count only, never on B)
   int jit_nsub = 1;              // lock-stepped sub-tiles per CTA in JIT kernels
-  bool jit_pipe = false;         // JIT TMA passes prefetch the next tile / defer store waits
+  int jit_pipe = -1;             // JIT TMA passes prefetch the next tile: 1 on, 0 off, -1 auto
+  bool cluster = false;          // cluster-resident: gbits = log2(CTAs per row), t = nloc
 
   uint64_t init_hmask = 0;         // leading H gates folded into the initial state (bits)
   uint64_t fold_mask = 0;          // bits whose leading U1 op is folded into the initial state
@@ -235,6 +236,8 @@ int u1_class(const std::vector<Constituent>& cons);  // plan.cpp: 0 general, 1 X
 tcx_status build_plan(int n, int P, const tcx_gate* gates, int64_t G, const double* mats,
                       int64_t nmat, tcx_dtype dtype, const tcx_build_opts* opts, Plan& plan,
                       std::string& err);
+// The step list of a sharded (or cluster-resident) program, identical on every rank
+std::vector<tcx_shard_step> shard_program(const Plan& P, const Binding& B, bool want_grad);
 tcx_status build_pauli(int n, int T, const uint8_t* codes, const double* w, Pauli& p,
                        std::string& err);
 std::shared_ptr<Binding> bind(Plan& plan, const Pauli& pauli);

@@ -343,6 +343,7 @@ struct Drv {
   CUresult (*launchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
                            unsigned, CUstream, void**, void**);
   CUresult (*funcSetAttribute)(CUfunction, CUfunction_attribute, int);
+  CUresult (*launchKernelEx)(const CUlaunchConfig*, CUfunction, void**, void**);
   CUresult (*tensorMapEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -362,6 +363,7 @@ Drv& drv() {
            get("cuModuleGetFunction", (void**)&D.moduleGetFunction) &&
            get("cuLaunchKernel", (void**)&D.launchKernel) &&
            get("cuFuncSetAttribute", (void**)&D.funcSetAttribute) &&
+           get("cuLaunchKernelEx", (void**)&D.launchKernelEx) &&
            get("cuTensorMapEncodeTiled", (void**)&D.tensorMapEncodeTiled);
   });
   return D;
@@ -499,16 +501,27 @@ bool fuse_last_of(const Plan& P, int kind, bool mega, const Binding* Bd) {
 tcx_status jit_prepare(Plan& P, int kind, bool mega, const Binding* Bd, bool fuse_last) {
   if (!P.jit_on) return TCX_OK;
   std::vector<std::string> keys;
+  if (P.cluster) {  // one megakernel (state kernels are not available for these plans)
+    if (!Bd || kind == 2) return TCX_OK;
+    std::string err;
+    if (!jit_build(P, {jit_key_cluster(Bd->hash, kind == 1 ? 1 : 0)}, err)) return fail(TCX_E_CUDA, err);
+    return TCX_OK;
+  }
   const int nP = (int)P.passes.size();
+  // kernels that compute lambda = H psi of unit 0 carry the binding (specialised terms)
+  auto lam_key = [&](int p, int km) {
+    return (Bd && kind != 2) ? jit_key_pass_lam(p, km, Bd->hash) : jit_key_pass(p, km);
+  };
   if (mega) {
-    keys.push_back(jit_key_pass(0, kind == 1 ? 2 : 0));
+    keys.push_back(lam_key(0, kind == 1 ? 2 : 0));
   } else {
     for (int p = 0; p < nP; ++p) {
       if (fuse_last && p == nP - 1) {  // last pass: forward + lambda + backward in one kernel
-        keys.push_back(jit_key_pass(p, 2));
+        keys.push_back(lam_key(p, 2));
         continue;
       }
-      keys.push_back(jit_key_pass(p, 0));
+      const bool lam_here = p == nP - 1 && P.gbits == 0;
+      keys.push_back(lam_here ? lam_key(p, 0) : jit_key_pass(p, 0));
       if (kind == 1) keys.push_back(jit_key_pass(p, 1));
     }
     if (Bd)
@@ -532,18 +545,24 @@ constexpr size_t kMaxBindings = 64;
 void evict_binding_locked(Plan& P, uint64_t hash) {  // P.mu held
   P.bindings.erase(hash);
   P.binding_use.erase(hash);
-  const std::string pre = jit_key_lambda(hash, 0).substr(0, 18);  // "L<16 hex>u"
+  // its kernels: lambda units "L<hex>u*", specialised pass kernels "p*k*h<hex>", cluster "C<hex>g*"
+  const std::string hex = jit_key_lambda(hash, 0).substr(1, 16);
+  auto mine = [&](const std::string& k) {
+    return (k[0] == 'L' || k[0] == 'C') ? k.compare(1, 16, hex) == 0
+                                        : (k.size() > 16 && k.compare(k.size() - 16, 16, hex) == 0 &&
+                                           k[k.size() - 17] == 'h');
+  };
   {
     std::lock_guard<std::mutex> jl(P.jit_mu);
     for (auto it = P.jit.begin(); it != P.jit.end();)
-      it = it->first.compare(0, pre.size(), pre) == 0 ? P.jit.erase(it) : std::next(it);
+      it = mine(it->first) ? P.jit.erase(it) : std::next(it);
   }
   bool synced = false;
   Drv& D = drv();
   for (auto& kv : P.dev) {
     DeviceTables* DT = kv.second.get();
     for (auto it = DT->jit.begin(); it != DT->jit.end();) {
-      if (it->first.compare(0, pre.size(), pre) != 0) {
+      if (!mine(it->first)) {
         ++it;
         continue;
       }
@@ -649,10 +668,11 @@ WsLayout ws_layout(const Plan& P, const Binding* Bd, int64_t B, int kind, bool h
   WsLayout w{};
   const size_t rs = P.dtype == TCX_C128 ? 8 : 4;
   const size_t N = size_t(1) << P.nloc;  // this rank's amplitudes (= 2^n unless sharded)
-  const int64_t S = P.tiles / tiles_per_cta(P);
+  // partial slots per theta row: tiles / CTA, or the CTAs of a cluster-resident row
+  const int64_t S = P.cluster ? ((int64_t)1 << P.gbits) : P.tiles / tiles_per_cta(P);
   const int EU = Bd ? (int)Bd->units.size() : 1;
-  w.mega = kind != K_STATE && P.passes.size() == 1 && EU == 1 && P.gbits == 0 &&
-           P.dblocks.empty() && !inputs;
+  w.mega = kind != K_STATE && ((P.passes.size() == 1 && EU == 1 && P.gbits == 0 &&
+                                P.dblocks.empty() && !inputs) || P.cluster);
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
@@ -808,10 +828,183 @@ struct OneStep {
   bool first_lambda;
 };
 
+// Cluster-resident plans (tcx_build_opts.cluster_bits): materialise the per-
+// theta matrices, one megakernel launch with a cluster of G = 2^g CTAs per theta row
+// (jit.cpp cluster_kernel: psi and lambda stay in registers, exchanges through distributed
+// shared memory), then the fixed-order finalize over the G per-CTA partials.
+tcx_status run_cluster(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, double* E,
+                       double* grad, void* ws, size_t ws_bytes, cudaStream_t st, int kind,
+                       const WsLayout* wl_in, const void* psi0, double* qim) {
+  if (kind == K_STATE || psi0 || qim)
+    return fail(TCX_E_UNSUPPORTED, "cluster-resident plans run tcx_expect_batch / tcx_grad_batch "
+                                   "only (the state never leaves the cluster's registers)");
+  if (B <= 0) return fail(TCX_E_INVALID, "B must be > 0");
+  if (!ws) return fail(TCX_E_INVALID, "null workspace");
+  if (P.P > 0 && !theta) return fail(TCX_E_INVALID, "null theta");
+  if (!E || (kind == K_GRAD && P.P > 0 && !grad)) return fail(TCX_E_INVALID, "null output");
+  if (kind == K_GRAD && !P.unitary)
+    return fail(TCX_E_UNSUPPORTED, "grad needs unitary payloads (adjoint applies U^dagger)");
+  if (!P.jit_on) return fail(TCX_E_UNSUPPORTED, "cluster-resident plans need per-circuit kernels (" + P.jit_note + ")");
+  if (!H) return fail(TCX_E_INVALID, "null pauli");
+  if (H->p.n != P.n) return fail(TCX_E_INVALID, "pauli n_qubits != circuit n_qubits");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(TCX_E_CUDA, "no CUDA device (tcx has no CPU fallback)");
+  DeviceTables* DT = nullptr;
+  tcx_status s = device_tables(P, DT);
+  if (s) return s;
+  std::shared_ptr<Binding> Bd;
+  BindDev bdv{nullptr, nullptr};
+  if ((s = binding_for(P, H, Bd, &bdv))) return s;
+  const WsLayout wl = wl_in ? *wl_in : ws_layout(P, Bd.get(), B, kind, false);
+  if (ws_bytes < wl.total)
+    return fail(TCX_E_INVALID, "workspace too small: need " + std::to_string(wl.total) +
+                                   " bytes, got " + std::to_string(ws_bytes));
+  const int G = 1 << P.gbits;
+  const int smem = jit_cluster_smem(P);
+  if (smem > 227 * 1024)
+    return fail(TCX_E_UNSUPPORTED, "cluster-resident plan needs " + std::to_string(smem) +
+                                       " B of shared memory per CTA (> 227 KB)");
+  const std::string key = jit_key_cluster(Bd->hash, kind == K_GRAD ? 1 : 0);
+  CUfunction jf = nullptr;
+  if ((s = jit_function(P, DT, key, &jf))) return s;
+  Drv& D = drv();
+  if (!D.launchKernelEx) return fail(TCX_E_CUDA, "cuLaunchKernelEx unavailable");
+  if ((size_t)smem > DT->jit_smem[key]) {
+    if (D.funcSetAttribute(jf, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem) != CUDA_SUCCESS ||
+        (G > 8 && D.funcSetAttribute(jf, CU_FUNC_ATTRIBUTE_NON_PORTABLE_CLUSTER_SIZE_ALLOWED, 1) != CUDA_SUCCESS))
+      return fail(TCX_E_CUDA, "cuFuncSetAttribute failed for " + jit_kernel_name(key));
+    DT->jit_smem[key] = smem;
+  }
+  char* W = (char*)ws;
+  const bool c128 = P.dtype == TCX_C128;
+  const int rs = c128 ? 8 : 4;
+  const int EU = (int)Bd->units.size();
+  const int64_t kMaxRows = 65535;
+  auto prof_begin = [&](ProfEntry& pe) -> tcx_status {
+    if (g_prof.on) {
+      CUDA_TRY(cudaEventCreate(&pe.a));
+      CUDA_TRY(cudaEventCreate(&pe.b));
+      CUDA_TRY(cudaEventRecord(pe.a, st));
+    }
+    return TCX_OK;
+  };
+  // ---- materialize per-theta matrices (as run())
+  for (int64_t b0 = 0; b0 < B && !P.mitems.empty(); b0 += kMaxRows) {
+    const int64_t rows = std::min(kMaxRows, B - b0);
+    MatArgs ma;
+    ma.items = (const MItem*)DT->mitems.p;
+    ma.nitems = (int)P.mitems.size();
+    ma.cons = (const DCons*)DT->dcons.p;
+    ma.fixed = (const double*)DT->fixed.p;
+    ma.theta = theta + b0 * P.P;
+    ma.P = P.P;
+    ma.mats = W + wl.mats + b0 * P.mat_total * rs;
+    ma.mat_total = P.mat_total;
+    dim3 g((ma.nitems + 127) / 128, (unsigned)rows);
+    if (c128)
+      materialize_kernel<double><<<g, 128, 0, st>>>(ma);
+    else
+      materialize_kernel<float><<<g, 128, 0, st>>>(ma);
+    CUDA_TRY(cudaGetLastError());
+  }
+  // ---- the megakernel: rows in chunks (grid.x = rows * G < 2^31)
+  PassArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.mats = W + wl.mats;
+  a.part = (double*)(W + wl.part);
+  a.epart = (double*)(W + wl.epart);
+  a.groups = bdv.groups;
+  a.pterms = bdv.pterms;
+  a.swb = (const uint32_t*)DT->swb.p;
+  for (int l = 0; l < P.t; ++l) a.W[l] = l;
+  a.n = P.nloc;
+  a.t = P.t;
+  a.h = P.h;
+  a.mat_total = P.mat_total;
+  a.acc_total = std::max(P.acc_total, 1);
+  a.e_units = EU;
+  a.mode = 0;
+  a.init_hmask = P.init_hmask;
+  a.init_amp = P.init_amp;
+  a.fold_active = 1;
+  ProfEntry pe{};
+  if ((s = prof_begin(pe))) return s;
+  const int64_t kMaxClusterRows = (int64_t)1 << 24;
+  for (int64_t b0 = 0; b0 < B; b0 += kMaxClusterRows) {
+    const int64_t rows = std::min(kMaxClusterRows, B - b0);
+    a.b0 = b0;
+    CUlaunchAttribute attr[1];
+    attr[0].id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
+    attr[0].value.clusterDim.x = (unsigned)G;
+    attr[0].value.clusterDim.y = 1;
+    attr[0].value.clusterDim.z = 1;
+    CUlaunchConfig cfg;
+    std::memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDimX = (unsigned)(rows * G);
+    cfg.gridDimY = 1;
+    cfg.gridDimZ = 1;
+    cfg.blockDimX = 1u << P.h;
+    cfg.blockDimY = 1;
+    cfg.blockDimZ = 1;
+    cfg.sharedMemBytes = (unsigned)smem;
+    cfg.hStream = (CUstream)st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    void* params[] = {&a};
+    const CUresult cr = D.launchKernelEx(&cfg, jf, params, nullptr);
+    if (cr != CUDA_SUCCESS)
+      return fail(TCX_E_CUDA, "cuLaunchKernelEx failed for " + jit_kernel_name(key) + " (CUresult " +
+                                  std::to_string((int)cr) + ")");
+  }
+  if (g_prof.on) {
+    CUDA_TRY(cudaEventRecord(pe.b, st));
+    double fl = 0;
+    for (auto& p : P.passes) fl += pass_flops(P, p, false) + (kind == K_GRAD ? pass_flops(P, p, true) : 0.0);
+    for (auto& u : Bd->units) fl += lambda_flops(*Bd, u);
+    pe.phase = 10;
+    pe.index = 0;
+    pe.flops = (double)B * (double)((int64_t)1 << P.n) * fl;
+    pe.bytes = (double)B * (P.mat_total * (double)rs + (double)G * 8.0 * (EU + (kind == K_GRAD ? P.acc_total : 0)));
+    g_prof.log.push_back(pe);
+  }
+  // ---- finalize over the G CTA partials of each row
+  for (int64_t b0 = 0; b0 < B; b0 += kMaxRows) {
+    const int64_t rows = std::min(kMaxRows, B - b0);
+    FinArgs f;
+    f.part = (const double*)(W + wl.part);
+    f.epart = (const double*)(W + wl.epart);
+    f.S = G;
+    f.K = std::max(P.acc_total, 1);
+    f.EU = EU;
+    f.gitems = (const GItem*)DT->gitems.p;
+    f.ngitems = (int)P.gitems.size();
+    f.cons = (const DCons*)DT->dcons.p;
+    f.fixed = (const double*)DT->fixed.p;
+    f.theta = theta;
+    f.P = P.P;
+    f.pptr = (const int32_t*)DT->pptr.p;
+    f.plist = (const int32_t*)DT->plist.p;
+    f.ncontrib = std::max(P.n_contrib, 1);
+    f.tot = (double*)(W + wl.tot);
+    f.contrib = (double*)(W + wl.contrib);
+    f.qcontrib = nullptr;
+    f.E = E;
+    f.grad = kind == K_GRAD && P.P > 0 ? grad : nullptr;
+    f.b0 = b0;
+    finalize_kernel<<<(unsigned)rows, 256, 0, st>>>(f);
+    CUDA_TRY(cudaGetLastError());
+  }
+  return TCX_OK;
+}
+
 tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, double* E,
                double* grad, void* state, void* ws, size_t ws_bytes, cudaStream_t st, int kind,
                const WsLayout* wl_in, const OneStep* one = nullptr, const void* psi0 = nullptr,
                bool keep_state = false, double* qim = nullptr) {
+  if (P.cluster)
+    return one ? fail(TCX_E_INVALID, "cluster-resident plans have no shard steps")
+               : run_cluster(P, H, theta, B, E, grad, ws, ws_bytes, st, kind, wl_in, psi0, qim);
   if (P.gbits > 0 && !one)
     return fail(TCX_E_INVALID, "sharded circuit (global_bits > 0): use tcx_shard_program/exec");
   auto want = [&](int k, int a) { return !one || (one->kind == k && one->arg == a); };
@@ -1043,8 +1236,10 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
     std::string jkey;
     if (P.jit_on) {
       const bool fwdk = (a.mode & (M_FWD | M_LAMBDA)) != 0, bwdk = (a.mode & M_BWD) != 0;
-      if (phase == 1 || phase == 3 || phase == 5 || phase == 9)
-        jkey = jit_key_pass(index, (fwdk && bwdk) ? 2 : (bwdk ? 1 : 0));
+      if (phase == 1 || phase == 3 || phase == 5 || phase == 9) {
+        const int km = (fwdk && bwdk) ? 2 : (bwdk ? 1 : 0);
+        jkey = ((a.mode & M_LAMBDA) && Bd) ? jit_key_pass_lam(index, km, Bd->hash) : jit_key_pass(index, km);
+      }
       else if (phase == 2 && Bd)
         jkey = jit_key_lambda(Bd->hash, index);
     }
@@ -1299,42 +1494,6 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
   return TCX_OK;
 }
 
-// The fixed step list of a sharded program (identical on every rank): materialise, forward
-// passes with an EXCHANGE between segments, lambda units (those flipping global qubits run
-// after an exchange), backward passes mirrored, finalise.
-std::vector<tcx_shard_step> shard_program(const Plan& P, const Binding& Bdr, bool want_grad) {
-  const Binding* Bd = &Bdr;
-  std::vector<tcx_shard_step> v;
-  auto add = [&](int k, int a) { v.push_back({k, a}); };
-  const int nP = (int)P.passes.size();
-  add(TCX_STEP_MATERIALIZE, 0);
-  for (int p = 0; p < nP; ++p) {
-    if (p > 0 && P.passes[p].seg != P.passes[p - 1].seg) add(TCX_STEP_EXCHANGE, 1);
-    add(TCX_STEP_FWD, p);
-  }
-  const int x = want_grad ? 3 : 1;  // exchange psi (+ lambda once it exists)
-  bool any_lam = false;
-  for (int u = 0; u < (int)Bd->units.size(); ++u)
-    if (!Bd->units[u].swapped) {
-      add(TCX_STEP_LAMBDA, u);
-      any_lam = true;
-    }
-  bool sw = false;
-  for (int u = 0; u < (int)Bd->units.size(); ++u)
-    if (Bd->units[u].swapped) {
-      if (!sw) add(TCX_STEP_EXCHANGE, any_lam ? x : 1);
-      sw = true;
-      add(TCX_STEP_LAMBDA, u);
-    }
-  if (sw && want_grad) add(TCX_STEP_EXCHANGE, x);  // back to the backward's layout
-  if (want_grad)
-    for (int p = nP - 1; p >= 0; --p) {
-      add(TCX_STEP_BWD, p);
-      if (p > 0 && P.passes[p].seg != P.passes[p - 1].seg) add(TCX_STEP_EXCHANGE, 3);
-    }
-  add(TCX_STEP_FINALIZE, 0);
-  return v;
-}
 
 }  // namespace
 
@@ -1686,6 +1845,7 @@ tcx_status tcx_circuit_info(const tcx_circuit* circ, const tcx_pauli* pauli, tcx
   o->dense_k = P.dense_k;
   o->dense_blocks = (int)P.dblocks.size();
   o->init_h = __builtin_popcountll(P.init_hmask);
+  o->cluster_bits = P.cluster ? P.gbits : 0;
   if (!P.dblocks.empty()) {  // the trailing E / lambda pass has no gates: no backward launch
     int nb = 0;
     for (auto& p : P.passes) nb += p.ops.empty() ? 0 : 1;
@@ -1740,6 +1900,7 @@ tcx_status tcx_shard_program(const tcx_circuit* circ, const tcx_pauli* pauli, in
   std::shared_ptr<Binding> Bd;
   tcx_status s = binding_for(P, pauli, Bd, nullptr);
   if (s) return s;
+  if (P.gbits == 0 || P.cluster) return fail(TCX_E_INVALID, "circuit is not sharded (global_bits = 0)");
   const std::vector<tcx_shard_step> v = shard_program(P, *Bd, want_grad != 0);
   *n = (int32_t)v.size();
   if (steps)
@@ -1754,7 +1915,7 @@ tcx_status tcx_shard_exec(const tcx_circuit* circ, const tcx_pauli* pauli, int32
   g_err.clear();
   if (!circ || !step) return fail(TCX_E_INVALID, "null argument");
   Plan& P = const_cast<tcx_circuit*>(circ)->plan;
-  if (P.gbits == 0) return fail(TCX_E_INVALID, "circuit is not sharded (global_bits = 0)");
+  if (P.gbits == 0 || P.cluster) return fail(TCX_E_INVALID, "circuit is not sharded (global_bits = 0)");
   if (rank < 0 || rank >= (1 << P.gbits)) return fail(TCX_E_INVALID, "rank out of range");
   if (step->kind == TCX_STEP_EXCHANGE) return fail(TCX_E_INVALID, "exchange steps run in the caller");
   OneStep one{step->kind, step->arg, rank, false};
@@ -1818,6 +1979,10 @@ tcx_status tcx_launch_count(const tcx_circuit* circ, const tcx_pauli* pauli, int
   const int kind = want_grad ? K_GRAD : K_EXPECT;
   WsLayout wl = ws_layout(P, Bd.get(), B, kind, false);
   auto chunks = [](int64_t rows) { return (rows + 65534) / 65535; };  // grid.y chunks
+  if (P.cluster) {  // materialize, the cluster megakernel, finalize
+    *launches = (int32_t)((P.mitems.empty() ? 0 : chunks(B)) + ((B + (1 << 24) - 1) >> 24) + chunks(B));
+    return TCX_OK;
+  }
   // mirrors run(): `once` launches, `perB` per row chunk of the whole batch, `perG` per row
   // chunk of every L2 row group (all rows when groups are off)
   int64_t once = 0, perB = 0, perG = 0;

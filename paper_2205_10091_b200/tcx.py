@@ -46,7 +46,7 @@ class tcx_build_opts(ctypes.Structure):
                 ("coalesce_bits", ctypes.c_int32), ("max_ops_per_pass", ctypes.c_int32),
                 ("jit", ctypes.c_int32), ("global_bits", ctypes.c_int32),
                 ("dense_k", ctypes.c_int32), ("q_grad", ctypes.c_int32),
-                ("l2_rows", ctypes.c_int32)]
+                ("l2_rows", ctypes.c_int32), ("cluster_bits", ctypes.c_int32)]
 
 
 class tcx_plan_info(ctypes.Structure):
@@ -55,7 +55,7 @@ class tcx_plan_info(ctypes.Structure):
         "threads_per_tile", "n_ops", "fwd_passes", "lambda_passes", "bwd_passes", "stages",
         "unitary", "relabeled", "jit", "global_bits", "segments")] + [(f, ctypes.c_int64) for f in (
             "tiles_per_state", "acc_slots", "mat_reals")] + [(f, ctypes.c_int32) for f in (
-            "dense_k", "dense_blocks", "init_h")]
+            "dense_k", "dense_blocks", "init_h", "cluster_bits")]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -67,7 +67,7 @@ class tcx_kernel_time(ctypes.Structure):
 
 
 PHASES = {0: "materialize", 1: "forward", 2: "lambda", 3: "backward", 4: "finalize", 5: "fused",
-          6: "dense", 7: "dense_backward", 8: "exchange", 9: "fused_last"}
+          6: "dense", 7: "dense_backward", 8: "exchange", 9: "fused_last", 10: "cluster"}
 
 
 class tcx_shard_step(ctypes.Structure):
@@ -166,7 +166,7 @@ class Circuit:
     def __init__(self, circ, dtype: str = "c64", tile_bits: int = 0, reg_bits: int = 0,
                  coalesce_bits: int = 0, max_ops_per_pass: int = 0, jit: bool = True,
                  global_bits: int = 0, gates=None, dense_k: int = 0, q_grad: bool = False,
-                 l2_rows: int = 0):
+                 l2_rows: int = 0, cluster_bits: int = 0):
         names, q0, q1, param, coeff, moff, mats = circ.arrays()
         self.n = circ.n
         self.P = circ.n_params
@@ -178,7 +178,8 @@ class Circuit:
             mats = np.zeros(2)
         self._mats = mats
         opts = tcx_build_opts(tile_bits, reg_bits, coalesce_bits, max_ops_per_pass,
-                              0 if jit else -1, global_bits, dense_k, 1 if q_grad else 0, l2_rows)
+                              0 if jit else -1, global_bits, dense_k, 1 if q_grad else 0, l2_rows,
+                              cluster_bits)
         self.global_bits = global_bits
         h = _vp()
         _check(_lib.tcx_circuit_build(self.n, self.P, self._gates, self.G,

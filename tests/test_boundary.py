@@ -227,3 +227,20 @@ def test_psi_h_dpsi_needs_dense_plan():
                                  ctypes.c_void_p(x.ctypes.data), ctypes.cast(buf, ctypes.c_void_p),
                                  len(buf), None)
     assert rc == 2 and "dense_k" in m.last_error()
+
+
+def test_cluster_plan_options():
+    """cluster_bits: one tile per CTA, 2^g partial slots, option validation."""
+    from paper_2205_10091_b200 import tcx
+    c, H = W.hea(17, 2), W.heisenberg(17)
+    C = tcx.Circuit(c, "c64", cluster_bits=4)
+    i = C.info(tcx.Pauli(H))
+    assert i["cluster_bits"] == 4 and i["tile_bits"] == 13 and i["threads_per_tile"] == 512
+    assert i["tiles_per_state"] == 1 and i["segments"] >= 1
+    for bad in ({"cluster_bits": 5}, {"cluster_bits": 3, "global_bits": 1}):
+        with pytest.raises(tcx.TcxError):
+            tcx.Circuit(c, "c64", **bad)
+    with pytest.raises(tcx.TcxError):  # 2^14 complex64 amplitudes do not fit one CTA's registers
+        tcx.Circuit(W.hea(17, 1), "c64", cluster_bits=3)
+    with pytest.raises(tcx.TcxError):  # complex128: at most 2^12 per CTA
+        tcx.Circuit(W.hea(16, 1), "c128", cluster_bits=3)
