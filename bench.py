@@ -130,6 +130,19 @@ def cpu_baseline(circ, H, theta, mode, name, max_rows=0):
     oracle (closed-form pinned instead) and cfg4 has B = 1 (row-parallel OpenMP cannot use
     more than one core there), so those report the single-thread figure only."""
     nproc, model = host_cpu()
+    if name.startswith("cfg4"):
+        # B = 1 and 8,900 gates on 2^30 amplitudes: hours in the oracle.  Time one layer of the
+        # same generator at n = 26 on one thread and scale linearly (the oracle's cost is gates x
+        # amplitudes): x 2^(n-26) amplitudes x layers
+        layers = 200
+        c1 = W.random_deep_circuit(26, 1, 4)
+        t1 = cpu_oracle_rows(c1, W.pauli_sum(26, [({0: "Z"}, 1.0)]), np.zeros((1, 0)), 1, "expect")
+        est = t1 * (1 << (circ.n - 26)) * layers
+        return {"value": 1.0 / est, "unit": "circuits/s", "cores": 1, "kind": "oracle",
+                "nproc": nproc, "cpu_model": model,
+                "sample": f"extrapolated: 1 layer of the cfg4 generator at n = 26 took {t1:.1f} s on one "
+                          f"thread, x 2^{circ.n - 26} amplitudes x {layers} layers = {est:.0f} s per circuit "
+                          "(B = 1: the oracle parallelises over rows only)"}
     if circ.n > 28:
         return {"value": None, "unit": "circuits/s", "cores": 0, "kind": "oracle",
                 "nproc": nproc, "cpu_model": model,
