@@ -109,6 +109,24 @@ def cpu_oracle_rows(circ, H, theta, threads, mode="grad"):
     return time.perf_counter() - t0
 
 
+def survey_flop_model(circ, H, B, ms_step, alu_peak):
+    """SURVEY §8(d)'s ALU flop model for a whole <H>+grad step, beside the library's own
+    per-kernel model: 6 flop/amp per rotation forward (structured 2x2), 0 for CNOT/CZ/SWAP,
+    15 flop/amp per parameterised gate backward (U^dagger on psi and lambda + the
+    Im<lambda|G|psi> term), 4 flop/amp per Pauli term for lambda = H psi.  Fraction = model
+    flops / step time / the FP32 (FP64) FMA peak."""
+    amps = float(1 << circ.n)
+    rot = sum(1 for g in circ.gates if g.name in ("rx", "ry", "rz", "rxx", "ryy", "rzz", "u1", "rrot"))
+    par = sum(1 for g in circ.gates if g.param >= 0)
+    per_amp = 6.0 * rot + 15.0 * par + 4.0 * len(H.weights)
+    fl = per_amp * amps * B
+    ach = fl / (ms_step / 1e3)
+    return {"flops_per_step": fl, "achieved_tflops": ach / 1e12, "peak_tflops": alu_peak / 1e12,
+            "frac": ach / alu_peak,
+            "model": "SURVEY 8(d): 6 flop/amp per rotation fwd, 15 per parameterised gate bwd, "
+                     "4 per Pauli term; whole step (all kernels) / measured FMA peak"}
+
+
 def host_cpu():
     """(logical cores, CPU model) of this host, recorded with every oracle figure."""
     model = "unknown"
@@ -433,6 +451,8 @@ def main():
     kernel_split = {k: {"ms": v[0] / prof_steps, "launches_per_step": v[3] / prof_steps,
                         "tflops": v[1] / max(v[0], 1e-9) / 1e9, "gbs": v[2] / max(v[0], 1e-9) / 1e6}
                     for k, v in by.items()}
+    if roof is not None and mode == "grad" and roof["bound"] == "alu":
+        roof["survey_model"] = survey_flop_model(circ, H, B, ms / args.steps, alu_peak)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

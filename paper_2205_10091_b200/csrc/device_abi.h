@@ -92,6 +92,7 @@ struct PassArgs {
   double init_amp;         //   these bits, amplitude init_amp = 2^(-popc/2) (plan.cpp)
   int fold_active;         // 1: the call starts from |0..0>, so leading U1 ops folded into
                            //   the product initial state are skipped in forward passes (JIT)
+  const uint8_t* cut[15];  // LUT cut tables: c(r) per local index (plan.cpp, JIT kernels)
 };
 
 struct SmemLayout {

@@ -1308,6 +1308,27 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
             kt.pad = o.lut && o.terms[i].w < 0 ? 1 : 0;  // LUT: sign of the term's weight
             P.kterms.push_back(kt);
           }
+          // Cut table: a LUT op's odd-parity count c(r) depends only on the index r and the
+          // op's (mask, sign) set -- theta- and row-independent -- so the JIT kernels read it
+          // from a per-plan byte table (2^n entries, L2-resident for n <= 26) instead of a
+          // popcount per term (QAOA: every cost layer shares one table)
+          static const bool no_cut = getenv("TCX_NO_CUT_TABLE") != nullptr;
+          if (o.lut && !no_cut && P.gbits == 0 && P.nloc <= kMaxCutBits && o.terms.size() < 256) {
+            std::vector<std::pair<uint64_t, int>> key;
+            for (size_t i = 0; i < o.terms.size(); ++i)
+              key.push_back({o.terms[i].mask, o.terms[i].w < 0 ? 1 : 0});
+            std::sort(key.begin(), key.end());
+            int id = -1;
+            for (size_t c2 = 0; c2 < P.cut_sets.size(); ++c2)
+              if (P.cut_sets[c2] == key) id = (int)c2;
+            // at most 15 tables (4 bits in KOp::cbit) and 1 GB of them
+            const size_t max_tabs = std::min<size_t>(15, ((size_t)1 << 30) >> P.nloc);
+            if (id < 0 && P.cut_sets.size() < max_tabs) {
+              id = (int)P.cut_sets.size();
+              P.cut_sets.push_back(key);
+            }
+            if (id >= 0) ko.cbit |= (uint8_t)((id + 1) << 4);
+          }
         }
         int na = op_accs(o);
         if (na > 0) {

@@ -20,6 +20,7 @@ namespace tcx {
 constexpr int kMaxQubits = 40;
 constexpr int kMaxTileBits = 15;
 constexpr int kMaxRegBits = 4;
+constexpr int kMaxCutBits = 26;  // cut tables (bytes per amplitude index) up to 64 MB
 
 // One original 1-qubit gate folded into a fused U1 op (applied in list order).
 struct Constituent {
@@ -192,6 +193,7 @@ struct Plan {
   int64_t tiles = 1;             // 2^(n - t)
   int tpc = 1;                   // tiles per CTA (depends on the tile count only, never on B)
   int jit_nsub = 1;              // lock-stepped sub-tiles per CTA in JIT kernels
+  std::vector<std::vector<std::pair<uint64_t, int>>> cut_sets;  // LUT cut tables (mask, sign)
   int jit_pipe = -1;             // JIT TMA passes prefetch the next tile: 1 on, 0 off, -1 auto
   bool cluster = false;          // cluster-resident: gbits = log2(CTAs per row), t = nloc
 

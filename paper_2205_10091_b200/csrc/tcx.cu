@@ -281,6 +281,17 @@ __global__ void hadamard_bit_kernel(Cx<Real>* psi, int n, int bit, int64_t pairs
   s[r1] = Cx<Real>{k * (x0.x - x1.x), k * (x0.y - x1.y)};
 }
 
+// cut table of a LUT op's (mask, sign) set: c(r) = #{k : parity(r & m_k) xor s_k odd}
+__global__ void cut_table_kernel(uint8_t* out, int64_t N, const uint64_t* masks, const int* signs,
+                                 int T) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < N;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    int c = 0;
+    for (int k = 0; k < T; ++k) c += (__popcll((uint64_t)r & masks[k]) & 1) ^ signs[k];
+    out[r] = (uint8_t)c;
+  }
+}
+
 // gather physical -> paper index order (only when SWAP relabels moved qubits)
 template <typename Real>
 __global__ void export_kernel(const Cx<Real>* src, Cx<Real>* dst, int n, int64_t total,
@@ -309,6 +320,7 @@ namespace tcx {
 struct DeviceTables {
   DevBuf kops, kterms, kstages, mitems, dcons, gitems, pptr, plist, fixed, layout, swb;
   DevBuf dblocks, dgates, dpblocks;  // dense k-qubit blocks (dense.cuh)
+  DevBuf cut[15];                    // LUT cut tables (Plan::cut_sets), 2^nloc bytes each
   std::map<std::string, CUfunction> jit;   // key (jit.h)
   std::map<std::string, size_t> jit_smem;  // dynamic smem opted in per function
   std::map<std::string, CUmodule> jit_mod;  // key -> its module (unloaded on eviction)
@@ -441,6 +453,22 @@ tcx_status device_tables(Plan& P, DeviceTables*& out) {
   if ((s = upload(T->dblocks, P.dblocks)) || (s = upload(T->dgates, P.dgates)) ||
       (s = upload(T->dpblocks, pbl)))
     return s;
+  for (size_t c = 0; c < P.cut_sets.size() && c < 15; ++c) {  // built once per plan and device
+    std::vector<uint64_t> m;
+    std::vector<int> sg;
+    for (auto& kv : P.cut_sets[c]) {
+      m.push_back(kv.first);
+      sg.push_back(kv.second);
+    }
+    DevBuf dm, ds;
+    if ((s = upload(dm, m)) || (s = upload(ds, sg))) return s;
+    const int64_t N = (int64_t)1 << P.nloc;
+    CUDA_TRY(cudaMalloc(&T->cut[c].p, (size_t)N));
+    cut_table_kernel<<<(unsigned)std::min<int64_t>(4096, (N + 255) / 256), 256>>>(
+        (uint8_t*)T->cut[c].p, N, (const uint64_t*)dm.p, (const int*)ds.p, (int)m.size());
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaDeviceSynchronize());  // dm / ds are freed on return
+  }
   out = T.get();
   P.dev[dev] = T;
   return TCX_OK;
@@ -1155,6 +1183,7 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
     a.init_hmask = P.init_hmask;
     a.init_amp = P.init_amp;
     a.fold_active = psi0 ? 0 : 1;
+    for (int c = 0; c < 15; ++c) a.cut[c] = (const uint8_t*)DT->cut[c].p;
   };
   auto set_pass = [&](PassArgs& a, const PassInfo& p, bool with_ops) {
     a.stages = (const KStage*)DT->kstages.p + p.stage_begin;

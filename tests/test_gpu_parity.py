@@ -277,15 +277,15 @@ def test_hea_zero_theta_n20(tc):
 # ------------------------------------------------------------ full-size cfg2
 @pytest.mark.slow
 def test_cfg2_full_batch_sampled_rows(tc):
-    """configs[1] at full size in the bench launch configuration (B=1024, c64); two
+    """configs[1] at full size in the bench launch configuration (B=1024, c64); four
     sampled rows checked against the oracle one by one, all rows checked for the
     theta-independent invariant |E| <= |H|_1 and finiteness."""
     name, c, H, th, dt = W.config(1)
     E, G, _ = run_grad(tc, c, H, th, dt)
     assert np.isfinite(E).all() and np.isfinite(G).all()
     assert (np.abs(E) <= H.l1).all()
-    rows = [0, 777]
-    Er, Gr = orc.value_grad_batch(c, H, th[rows], nthreads=2)
+    rows = [0, 333, 777, 1023]  # both ends of the batch and two inside it
+    Er, Gr = orc.value_grad_batch(c, H, th[rows], nthreads=len(rows))
     check_E(E[rows], Er, H, dt, "cfg2 E")
     check_grad(G[rows], Gr, H, c, dt, "cfg2 grad")
 
@@ -293,7 +293,7 @@ def test_cfg2_full_batch_sampled_rows(tc):
 @pytest.mark.slow
 def test_cfg3_full_batch_sampled_row(tc):
     """configs[2] at full size in the bench launch configuration (QAOA n=24, p=5, B=256,
-    c64): E and the (gamma, beta) gradient of one sampled row against the oracle; every
+    c64): E and the (gamma, beta) gradient of three sampled rows against the oracle; every
     row satisfies 0 <= <C> <= |E| (the cut value is a count of edges)."""
     name, c, H, th, dt = W.config(2)
     E, G, _ = run_grad(tc, c, H, th, dt)
@@ -301,8 +301,8 @@ def test_cfg3_full_batch_sampled_row(tc):
     n_edges = float(H.weights[0]) * 2 if (H.codes[0] == 0).all() else None
     if n_edges:
         assert (E >= -1e-4).all() and (E <= n_edges + 1e-4).all()
-    rows = [131]
-    Er, Gr = orc.value_grad_batch(c, H, th[rows], nthreads=1)
+    rows = [0, 131, 255]
+    Er, Gr = orc.value_grad_batch(c, H, th[rows], nthreads=len(rows))
     check_E(E[rows], Er, H, dt, "cfg3 E")
     check_grad(G[rows], Gr, H, c, dt, "cfg3 grad")
 
