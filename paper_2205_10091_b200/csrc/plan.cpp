@@ -1312,8 +1312,10 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
           // op's (mask, sign) set -- theta- and row-independent -- so the JIT kernels read it
           // from a per-plan byte table (2^n entries, L2-resident for n <= 26) instead of a
           // popcount per term (QAOA: every cost layer shares one table)
-          static const bool no_cut = getenv("TCX_NO_CUT_TABLE") != nullptr;
-          if (o.lut && !no_cut && P.gbits == 0 && P.nloc <= kMaxCutBits && o.terms.size() < 256) {
+          // Measured slower on cfg3 (424 -> 352 circuits/s: the byte reads follow the stage
+          // mapping, so a warp's 32 lanes hit 32 L2 sectors per load), hence opt-in.
+          static const bool cut_on = getenv("TCX_CUT_TABLE") != nullptr;
+          if (o.lut && cut_on && P.gbits == 0 && P.nloc <= kMaxCutBits && o.terms.size() < 256) {
             std::vector<std::pair<uint64_t, int>> key;
             for (size_t i = 0; i < o.terms.size(); ++i)
               key.push_back({o.terms[i].mask, o.terms[i].w < 0 ? 1 : 0});
