@@ -576,7 +576,10 @@ def run_sharded(args, world, rank, local, dev):
                    "virtual_ranks": world == 1,
                    "comm": "NCCL (library-owned communicator)" if world > 1 else
                            "virtual ranks (in-place swap kernels, one GPU)",
-                   "plan": {k: info[k] for k in ("fwd_passes", "segments", "lambda_passes", "jit")},
+                   "plan": {k: info[k] for k in ("fwd_passes", "segments", "lambda_passes", "jit",
+                                                 "exchange_overlaps")},
+                   "exchange_overlap": "off (TCX_XCHG_NO_OVERLAP)" if os.environ.get("TCX_XCHG_NO_OVERLAP")
+                                       else "next pass runs by chunks as they land",
                    "exchanges_per_step": {"psi": nx1, "psi_and_lambda": nx3},
                    "jit_compile_s": round(t_jit, 2),
                    "l2": "inputs larger than L2 (2^%d amplitudes per rank)" % (n - g)},

@@ -152,6 +152,8 @@ typedef struct {
     int32_t dense_blocks;     /* dense k-qubit block passes (each one read+write of psi) */
     int32_t init_h;           /* leading H gates folded into the initial |+> state */
     int32_t cluster_bits;     /* cluster-resident plan: CTAs per theta row = 2^cluster_bits */
+    int32_t exchange_overlaps; /* sharded: exchanges whose next pass (forward or backward) runs
+                                  chunk by chunk as the exchange lands (overlap) */
 } tcx_plan_info;
 
 typedef struct tcx_circuit tcx_circuit;

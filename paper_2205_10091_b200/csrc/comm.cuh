@@ -27,6 +27,8 @@
 
 namespace {
 
+constexpr int kXChunksMax = 8;  // column chunks of an exchange overlapped with the next pass
+
 // ---- NCCL entry points (torch's libnccl when already loaded in the process, else the system one)
 struct NcclApi {
   bool ok = false;
@@ -84,17 +86,19 @@ NcclApi& nccl() {
       return fail(TCX_E_NCCL, std::string(#x) + ": " + nccl().errorString(r_));            \
   } while (0)
 
-// ---- virtual ranks: rank r's block k <-> rank k's block r for the G/2 pairs of XOR step s
+// ---- virtual ranks: rank r's block k <-> rank k's block r for the G/2 pairs of XOR step s,
+// restricted to the byte columns [col_off, col_off + col_bytes) of each block (a chunk)
 struct SwapArgs {
   char* base[64];  // each rank's psi (or lambda) buffer, [B][G][C] amplitudes
   int64_t row_bytes;    // N * amplitude bytes
-  int64_t block_bytes;  // C * amplitude bytes (multiple of 16)
+  int64_t block_bytes;  // C * amplitude bytes
+  int64_t col_off, col_bytes;  // chunk of each block (multiples of 16)
   int64_t B;
   int s;      // XOR step
   int hbit;   // highest set bit of s
 };
 __global__ void virtual_swap_kernel(const SwapArgs a) {
-  const int64_t vecs = a.block_bytes >> 4;
+  const int64_t vecs = a.col_bytes >> 4;
   const int64_t per_pair = vecs * a.B;
   const int pair = blockIdx.y;
   // the pair's lower rank: insert a zero at bit hbit of the pair index
@@ -104,8 +108,8 @@ __global__ void virtual_swap_kernel(const SwapArgs a) {
   for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < per_pair;
        u += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = u / vecs, v = u - b * vecs;
-    uint4* x = reinterpret_cast<uint4*>(a.base[r] + b * a.row_bytes + k * a.block_bytes) + v;
-    uint4* y = reinterpret_cast<uint4*>(a.base[k] + b * a.row_bytes + r * a.block_bytes) + v;
+    uint4* x = reinterpret_cast<uint4*>(a.base[r] + b * a.row_bytes + k * a.block_bytes + a.col_off) + v;
+    uint4* y = reinterpret_cast<uint4*>(a.base[k] + b * a.row_bytes + r * a.block_bytes + a.col_off) + v;
     const uint4 tx = *x, ty = *y;
     *x = ty;
     *y = tx;
@@ -134,12 +138,15 @@ struct tcx_comm {
   cudaEvent_t ev_go = nullptr, ev_done = nullptr, ev_recv[2] = {nullptr, nullptr},
               ev_copy[2] = {nullptr, nullptr};
   size_t chunk = (size_t)256 << 20;  // staging chunk (bytes); two are resident
+  cudaEvent_t ev_chunk[kXChunksMax] = {};  // overlapped exchanges: chunk c has landed
   void* hsend = nullptr;             // host transport: pinned staging
   void* hrecv = nullptr;
   size_t hbytes = 0;
   ~tcx_comm() {
     if (nc) nccl().commDestroy(nc);
     for (cudaEvent_t e : {ev_go, ev_done, ev_recv[0], ev_recv[1], ev_copy[0], ev_copy[1]})
+      if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : ev_chunk)
       if (e) cudaEventDestroy(e);
     if (cs) cudaStreamDestroy(cs);
     if (ks) cudaStreamDestroy(ks);
@@ -157,6 +164,7 @@ tcx_status comm_streams(tcx_comm* c) {
   for (cudaEvent_t* e : {&c->ev_go, &c->ev_done, &c->ev_recv[0], &c->ev_recv[1], &c->ev_copy[0],
                          &c->ev_copy[1]})
     CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  for (cudaEvent_t& e : c->ev_chunk) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   if (const char* e = getenv("TCX_XCHG_CHUNK_MB")) c->chunk = (size_t)std::max(1, atoi(e)) << 20;
   return TCX_OK;
 }
@@ -181,9 +189,30 @@ ShardWs shard_ws(const Plan& P, const Binding* Bd, const tcx_comm* c, int64_t B,
   return s;
 }
 
-// One EXCHANGE of the buffers at byte offset `boff` inside each rank's workspace.
-tcx_status exchange(tcx_comm* c, const Plan& P, char* W, const ShardWs& sw, size_t boff, int64_t B,
-                    cudaStream_t st) {
+// EXCHANGE of the buffers at byte offset `boff` inside each rank's workspace, for the byte
+// columns [c0, c1) of every block (the whole block, or one chunk of an exchange that overlaps
+// the next pass).  xchg_begin orders the exchange streams after everything already queued on
+// the caller's stream; xchg_cols enqueues the data movement on them (virtual: swap kernels on
+// the exchange stream; NCCL: grouped send / recv on it and staging copies on the copy stream;
+// host: synchronous on the caller's stream); xchg_mark records `ev` once the columns landed.
+tcx_status xchg_begin(tcx_comm* c, cudaStream_t st) {
+  if (c->kind == TCX_COMM_HOST) return TCX_OK;
+  CUDA_TRY(cudaEventRecord(c->ev_go, st));
+  CUDA_TRY(cudaStreamWaitEvent(c->cs, c->ev_go, 0));
+  CUDA_TRY(cudaStreamWaitEvent(c->ks, c->ev_go, 0));
+  return TCX_OK;
+}
+tcx_status xchg_mark(tcx_comm* c, cudaEvent_t ev, cudaStream_t st) {
+  if (c->kind == TCX_COMM_HOST) return TCX_OK;  // already complete on st
+  // both streams: the exchange stream (swaps / sends and receives) and the copy stream
+  CUDA_TRY(cudaEventRecord(c->ev_done, c->cs));
+  CUDA_TRY(cudaStreamWaitEvent(c->ks, c->ev_done, 0));
+  CUDA_TRY(cudaEventRecord(ev, c->ks));
+  (void)st;
+  return TCX_OK;
+}
+tcx_status xchg_cols(tcx_comm* c, const Plan& P, char* W, const ShardWs& sw, size_t boff, int64_t B,
+                     int64_t c0, int64_t c1, int& it, cudaStream_t st) {
   const int G = 1 << P.gbits;
   const size_t esz = P.dtype == TCX_C128 ? 16 : 8;
   const int64_t N = (int64_t)1 << P.nloc;
@@ -193,22 +222,24 @@ tcx_status exchange(tcx_comm* c, const Plan& P, char* W, const ShardWs& sw, size
     for (int r = 0; r < G; ++r) a.base[r] = W + r * sw.per_rank + boff;
     a.row_bytes = N * (int64_t)esz;
     a.block_bytes = Cb;
+    a.col_off = c0;
+    a.col_bytes = c1 - c0;
     a.B = B;
     for (int s = 1; s < G; ++s) {
       a.s = s;
       a.hbit = 31 - __builtin_clz(s);
-      const int64_t per_pair = (Cb >> 4) * B;
+      const int64_t per_pair = (a.col_bytes >> 4) * B;
       const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((per_pair + 255) / 256,
                                                                            148 * 8 / std::max(1, G / 2)));
-      virtual_swap_kernel<<<dim3(gx, G / 2), 256, 0, st>>>(a);
+      virtual_swap_kernel<<<dim3(gx, G / 2), 256, 0, c->cs>>>(a);
       CUDA_TRY(cudaGetLastError());
     }
     return TCX_OK;
   }
   char* buf = W + boff;
   const int r = c->rank;
-  // rows of one chunk: the whole block when it fits, else a column range of every row
-  const int64_t cols = std::max<int64_t>(16, std::min<int64_t>(Cb, (int64_t)c->chunk / B) & ~(int64_t)15);
+  // rows of one staging chunk: the whole column range when it fits, else a sub-range
+  const int64_t cols = std::max<int64_t>(16, std::min<int64_t>(c1 - c0, (int64_t)c->chunk / B) & ~(int64_t)15);
   if (c->kind == TCX_COMM_HOST) {
     const size_t need = (size_t)B * cols;
     if (c->hbytes < need) {
@@ -222,14 +253,14 @@ tcx_status exchange(tcx_comm* c, const Plan& P, char* W, const ShardWs& sw, size
     }
     for (int s = 1; s < G; ++s) {
       const int peer = r ^ s;
-      for (int64_t c0 = 0; c0 < Cb; c0 += cols) {
-        const int64_t w = std::min(cols, Cb - c0);
-        CUDA_TRY(cudaMemcpy2DAsync(c->hsend, w, buf + peer * Cb + c0, N * esz, w, B,
+      for (int64_t x0 = c0; x0 < c1; x0 += cols) {
+        const int64_t w = std::min(cols, c1 - x0);
+        CUDA_TRY(cudaMemcpy2DAsync(c->hsend, w, buf + peer * Cb + x0, N * esz, w, B,
                                    cudaMemcpyDeviceToHost, st));
         CUDA_TRY(cudaStreamSynchronize(st));
         if (c->fn(c->user, peer, c->hsend, c->hrecv, (size_t)(w * B)) != 0)
           return fail(TCX_E_NCCL, "host exchange callback failed");
-        CUDA_TRY(cudaMemcpy2DAsync(buf + peer * Cb + c0, N * esz, c->hrecv, w, w, B,
+        CUDA_TRY(cudaMemcpy2DAsync(buf + peer * Cb + x0, N * esz, c->hrecv, w, w, B,
                                    cudaMemcpyHostToDevice, st));
       }
     }
@@ -240,35 +271,40 @@ tcx_status exchange(tcx_comm* c, const Plan& P, char* W, const ShardWs& sw, size
   // moves chunk i into place while chunk i+1 is on the wire.
   NcclApi& A = nccl();
   char* stage[2] = {W + sw.stage, W + sw.stage + align256(c->chunk)};
-  CUDA_TRY(cudaEventRecord(c->ev_go, st));
-  CUDA_TRY(cudaStreamWaitEvent(c->cs, c->ev_go, 0));
-  CUDA_TRY(cudaStreamWaitEvent(c->ks, c->ev_go, 0));
-  int it = 0;
   for (int s = 1; s < G; ++s) {
     const int peer = r ^ s;
-    for (int64_t c0 = 0; c0 < Cb; c0 += cols, ++it) {
-      const int64_t w = std::min(cols, Cb - c0);
+    for (int64_t x0 = c0; x0 < c1; x0 += cols, ++it) {
+      const int64_t w = std::min(cols, c1 - x0);
       const int sb = it & 1;
       if (it >= 2) CUDA_TRY(cudaStreamWaitEvent(c->cs, c->ev_copy[sb], 0));  // staging free
       NCCL_TRY(A.groupStart());
       for (int64_t b = 0; b < B; ++b) {
-        NCCL_TRY(A.send(buf + b * N * esz + peer * Cb + c0, (size_t)w, ncclUint8, peer, c->nc, c->cs));
+        NCCL_TRY(A.send(buf + b * N * esz + peer * Cb + x0, (size_t)w, ncclUint8, peer, c->nc, c->cs));
         NCCL_TRY(A.recv(stage[sb] + b * w, (size_t)w, ncclUint8, peer, c->nc, c->cs));
       }
       NCCL_TRY(A.groupEnd());
       CUDA_TRY(cudaEventRecord(c->ev_recv[sb], c->cs));
       CUDA_TRY(cudaStreamWaitEvent(c->ks, c->ev_recv[sb], 0));
-      CUDA_TRY(cudaMemcpy2DAsync(buf + peer * Cb + c0, N * esz, stage[sb], w, w, B,
-                                 cudaMemcpyDeviceToDevice, c->ks));
-      CUDA_TRY(cudaEventRecord(c->ev_copy[sb], c->ks));
       // the copy overwrites the block range just sent: ev_recv completes with the whole
       // group, sends included
+      CUDA_TRY(cudaMemcpy2DAsync(buf + peer * Cb + x0, N * esz, stage[sb], w, w, B,
+                                 cudaMemcpyDeviceToDevice, c->ks));
+      CUDA_TRY(cudaEventRecord(c->ev_copy[sb], c->ks));
     }
   }
-  CUDA_TRY(cudaEventRecord(c->ev_done, c->ks));
-  CUDA_TRY(cudaStreamWaitEvent(st, c->ev_done, 0));
-  CUDA_TRY(cudaEventRecord(c->ev_done, c->cs));
-  CUDA_TRY(cudaStreamWaitEvent(st, c->ev_done, 0));
+  return TCX_OK;
+}
+
+// One whole EXCHANGE (every column of every block), joined back into the caller's stream.
+tcx_status exchange(tcx_comm* c, const Plan& P, char* W, const ShardWs& sw, size_t boff, int64_t B,
+                    cudaStream_t st) {
+  const int64_t Cb = ((int64_t)1 << (P.nloc - P.gbits)) * (P.dtype == TCX_C128 ? 16 : 8);
+  int it = 0;
+  tcx_status s;
+  if ((s = xchg_begin(c, st)) || (s = xchg_cols(c, P, W, sw, boff, B, 0, Cb, it, st)) ||
+      (s = xchg_mark(c, c->ev_chunk[0], st)))
+    return s;
+  if (c->kind != TCX_COMM_HOST) CUDA_TRY(cudaStreamWaitEvent(st, c->ev_chunk[0], 0));
   return TCX_OK;
 }
 
@@ -340,25 +376,57 @@ tcx_status run_sharded(Plan& P, const tcx_pauli* H, tcx_comm* c, const double* t
   double* parts = (double*)(W + sw.parts);
   auto Ep = [&](int li) { return sw.local > 1 ? parts + (size_t)li * B * (1 + Pp) : E; };
   auto Gp = [&](int li) { return sw.local > 1 ? parts + (size_t)li * B * (1 + Pp) + B : grad; };
-  for (const tcx_shard_step& stp : prog) {
+  const bool no_overlap = getenv("TCX_XCHG_NO_OVERLAP") != nullptr;  // A/B switch, read per call
+  const int64_t Cb = ((int64_t)1 << (P.nloc - P.gbits)) * (P.dtype == TCX_C128 ? 16 : 8);
+  for (size_t si = 0; si < prog.size(); ++si) {
+    const tcx_shard_step& stp = prog[si];
     if (stp.kind == TCX_STEP_EXCHANGE) {
+      const bool both = (stp.arg & 2) && wl.lam;
+      // the next pass can start on chunk q while chunks q+1.. are still moving when its window
+      // leaves the chunk bits out (tcx.cu pass_chunkable; planned for by the layout search)
+      const tcx_shard_step* nx = si + 1 < prog.size() ? &prog[si + 1] : nullptr;
+      const bool overlap = !no_overlap && nx && (nx->kind == TCX_STEP_FWD || nx->kind == TCX_STEP_BWD) &&
+                           pass_chunkable(P, P.passes[nx->arg]) && c->kind != TCX_COMM_HOST;
       ProfEntry pe{};
+      cudaStream_t ps = c->kind == TCX_COMM_HOST ? st : c->cs;  // the exchange's own timeline
       if (g_prof.on) {
         CUDA_TRY(cudaEventCreate(&pe.a));
         CUDA_TRY(cudaEventCreate(&pe.b));
-        CUDA_TRY(cudaEventRecord(pe.a, st));
       }
-      if ((s = exchange(c, P, W, sw, wl.psi, B, st))) return s;
-      const bool both = (stp.arg & 2) && wl.lam;
-      if (both && (s = exchange(c, P, W, sw, wl.lam, B, st))) return s;
+      if (!overlap) {
+        if (g_prof.on) CUDA_TRY(cudaEventRecord(pe.a, st));
+        if ((s = exchange(c, P, W, sw, wl.psi, B, st))) return s;
+        if (both && (s = exchange(c, P, W, sw, wl.lam, B, st))) return s;
+        if (g_prof.on) CUDA_TRY(cudaEventRecord(pe.b, st));
+      } else {
+        const int nc = 1 << P.xchunk_bits;
+        int it = 0;
+        if ((s = xchg_begin(c, st))) return s;
+        if (g_prof.on) CUDA_TRY(cudaEventRecord(pe.a, ps));
+        for (int q = 0; q < nc; ++q) {
+          const int64_t c0 = Cb * q / nc, c1 = Cb * (q + 1) / nc;
+          if ((s = xchg_cols(c, P, W, sw, wl.psi, B, c0, c1, it, st))) return s;
+          if (both && (s = xchg_cols(c, P, W, sw, wl.lam, B, c0, c1, it, st))) return s;
+          if ((s = xchg_mark(c, c->ev_chunk[q], st))) return s;
+          if (g_prof.on && q == nc - 1) CUDA_TRY(cudaEventRecord(pe.b, c->ks));
+          CUDA_TRY(cudaStreamWaitEvent(st, c->ev_chunk[q], 0));
+          for (int li = 0; li < sw.local; ++li) {  // the next pass on chunk q of every rank
+            const int rank = sw.local > 1 ? li : c->rank;
+            OneStep one{nx->kind, nx->arg, rank, false, q};
+            if ((s = run(P, H, theta, B, Ep(li), Gp(li), nullptr, W + (size_t)li * sw.per_rank,
+                         sw.per_rank, st, kind, &wl, &one)))
+              return s;
+          }
+        }
+        ++si;  // that pass ran
+      }
       if (g_prof.on) {
-        CUDA_TRY(cudaEventRecord(pe.b, st));
         // bytes that change rank: (G-1)/G of every local state moved; virtual ranks read and
         // write each of them in HBM (swap kernel), a real rank sends its share over the link
         const double moved = (double)B * (double)((int64_t)1 << P.nloc) * (P.dtype == TCX_C128 ? 16 : 8) *
                              (double)(c->world - 1) / c->world * (both ? 2 : 1);
         pe.phase = 8;
-        pe.index = stp.arg;
+        pe.index = stp.arg | (overlap ? 4 : 0);
         pe.flops = 0;
         pe.bytes = sw.local > 1 ? 2.0 * moved * sw.local : moved;
         g_prof.log.push_back(pe);

@@ -93,7 +93,18 @@ struct PassArgs {
   int fold_active;         // 1: the call starts from |0..0>, so leading U1 ops folded into
                            //   the product initial state are skipped in forward passes (JIT)
   const uint8_t* cut[15];  // LUT cut tables: c(r) per local index (plan.cpp, JIT kernels)
+  // chunked launches (sharded exchange overlapped with the next pass): this launch covers the
+  // tiles whose tile-index bits [chunk_pos, chunk_pos + chunk_bits) equal chunk_val; the CTA's
+  // partial slot is b * cta_stride + cta_base + blockIdx.x (cta_stride = CTAs per full launch)
+  int chunk_pos, chunk_bits, chunk_val, cta_base;
+  int64_t cta_stride;
 };
+// tile index of a (possibly chunked) launch: the chunk value inserted at chunk_pos
+TCX_HD inline int64_t chunk_tile(int64_t t, int pos, int bits, int val) {
+  if (!bits) return t;
+  const int64_t lo = t & ((1ll << pos) - 1);
+  return ((t >> pos) << (pos + bits)) | ((int64_t)val << pos) | lo;
+}
 
 struct SmemLayout {
   int xb_psi, xb_lam, mats, wacc, cacc, stages, red, pb, total;

@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(512, 1) pass_kernel(const PassArgs a) {
   double e_acc = 0.0;
 
   for (int it = 0; it < a.tiles_per_cta; ++it) {
-    const int64_t tile = (int64_t)blockIdx.x * a.tiles_per_cta + it;
+    const int64_t tile = chunk_tile((int64_t)blockIdx.x * a.tiles_per_cta + it, a.chunk_pos, a.chunk_bits, a.chunk_val);
     uint64_t outer = 0;
     {
       int64_t tt = tile;
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(512, 1) pass_kernel(const PassArgs a) {
 
   // ------------------------------------------------------------- epilogue
   __syncthreads();
-  const int64_t cta = b * gridDim.x + blockIdx.x;
+  const int64_t cta = b * a.cta_stride + a.cta_base + blockIdx.x;
   if (kBwd && (mode & M_BWD)) {
     double* dst = a.part + cta * a.acc_total + a.acc_begin;
     for (int i = tid; i < a.acc_count; i += nthr) dst[i] = cacc[i];

@@ -307,6 +307,7 @@ struct Scheduler {
   // the greedy choice to the end of the schedule and the one finishing in the fewest passes
   // wins (ties: more work now).
   bool lookahead = false;
+  uint64_t forbid = 0;  // bits the next window must leave out (exchange chunk bits)
   bool tma_ok(uint64_t W) const { return tma_dims(nl, W, P.dtype == TCX_C128).rank > 0; }
   uint64_t choose_window() {
     std::vector<std::pair<double, uint64_t>> cand;
@@ -371,7 +372,8 @@ struct Scheduler {
       }
     };
     auto fill = [&](uint64_t W) {  // pad with lowest unused bits
-      for (int b = 0; b < n && popc64(W) < t; ++b) W |= 1ull << b;
+      for (int b = 0; b < n && popc64(W) < t; ++b)
+        if (!(forbid >> b & 1)) W |= 1ull << b;
       return W;
     };
     // (a) greedy growth by score
@@ -381,7 +383,7 @@ struct Scheduler {
         double cur = closure(W, nullptr), bs = -1;
         int bb = -1;
         for (int b = 0; b < n; ++b) {
-          if (W >> b & 1) continue;
+          if ((W >> b & 1) || (forbid >> b & 1)) continue;
           double s = closure(W | (1ull << b), nullptr);
           if (s > bs) {
             bs = s;
@@ -392,7 +394,7 @@ struct Scheduler {
           uint64_t miss = first_missing(W);
           uint64_t add = 0;
           for (int b = 0; b < n; ++b)
-            if (miss >> b & 1) {
+            if ((miss >> b & 1) && !(forbid >> b & 1)) {
               add = 1ull << b;
               break;
             }
@@ -412,7 +414,7 @@ struct Scheduler {
       uint64_t W = base;
       const uint64_t lmask = (n >= 64) ? ~0ull : ((1ull << n) - 1);
       for (int i = first; i < (int)P.ops.size() && popc64(W) < t; ++i) {
-        if (done[i] || (P.ops[i].need & ~lmask)) continue;  // global bits never enter a window
+        if (done[i] || (P.ops[i].need & ~lmask) || (P.ops[i].need & forbid)) continue;  // global bits never enter a window
         uint64_t nw = W | P.ops[i].need;
         if (popc64(nw) <= t) W = nw;
       }
@@ -422,7 +424,7 @@ struct Scheduler {
     for (int s = c; s + (t - c) <= n; ++s) {
       uint64_t W = base;
       for (int b = s; b < s + (t - c); ++b) W |= 1ull << b;
-      consider(W);
+      if (!(W & forbid)) consider(W);
     }
     return bestW;
   }
@@ -1077,10 +1079,22 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
   size_t left = P.ops.size();
   int seg = 0;
   bool swapped_last = false;
+  // exchange chunks (overlap of an exchange with the next pass, comm.cuh): the 2 local bits
+  // below the exchanged top g, kept out of the first window after each exchange when possible
+  P.xchunk_bits = (gb > 0 && !P.cluster && P.nloc - gb - 2 >= P.c + 2 && !getenv("TCX_NO_XCHUNK")) ? 2 : 0;
+  const uint64_t xmask = (P.xchunk_bits && P.xchunk_forbid)
+      ? (((1ull << P.xchunk_bits) - 1) << (P.nloc - gb - P.xchunk_bits)) : 0;
   while (left > 0) {
+    S.forbid = swapped_last ? xmask : 0;
     uint64_t W = S.choose_window();
     std::vector<int> list;
     S.closure(W, &list);
+    if (list.empty() && S.forbid) {  // nothing runs without the chunk bits: plain window
+      S.forbid = 0;
+      W = S.choose_window();
+      S.closure(W, &list);
+    }
+    S.forbid = 0;
     if (list.empty() && gb > 0 && !swapped_last) {
       // blocked on global qubits: exchange global <-> top-local bits, relabel what is left
       int perm[64];

@@ -854,7 +854,30 @@ cudaError_t dense_bwd(int K, DenseArgs& a, int S, int64_t rows, cudaStream_t st)
 struct OneStep {
   int kind, arg, rank;
   bool first_lambda;
+  int chunk = -1;  // >= 0: only the tiles of exchange chunk `chunk` (overlapped exchange)
 };
+
+// Exchange chunks (sharded plans): the top P.xchunk_bits local bits below the g exchanged ones
+// split every block into 2^xchunk_bits column ranges.  A pass whose window leaves those bits
+// out can start on chunk c as soon as chunk c of the exchange has landed.
+uint64_t xchunk_mask(const Plan& P) {
+  if (P.gbits == 0 || P.cluster || P.xchunk_bits == 0) return 0;
+  const int hi = P.nloc - P.gbits;
+  return (((1ull << P.xchunk_bits) - 1) << (hi - P.xchunk_bits));
+}
+bool pass_chunkable(const Plan& P, const PassInfo& p) {
+  const uint64_t m = xchunk_mask(P);
+  if (!m || (p.wmask & m)) return false;
+  const int64_t S = P.tiles / P.tpc;
+  return S % (1ll << P.xchunk_bits) == 0;
+}
+// position of the lowest chunk bit in the tile index (non-window local bits, increasing)
+int chunk_tile_pos(const Plan& P, uint64_t wmask) {
+  const int lo = P.nloc - P.gbits - P.xchunk_bits;
+  int k = 0;
+  for (int b = 0; b < lo; ++b) k += (wmask >> b & 1) ? 0 : 1;
+  return k;
+}
 
 // Cluster-resident plans (tcx_build_opts.cluster_bits): materialise the per-
 // theta matrices, one megakernel launch with a cluster of G = 2^g CTAs per theta row
@@ -1184,6 +1207,9 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
     a.init_amp = P.init_amp;
     a.fold_active = psi0 ? 0 : 1;
     for (int c = 0; c < 15; ++c) a.cut[c] = (const uint8_t*)DT->cut[c].p;
+    a.cta_stride = S;
+    a.cta_base = 0;
+    a.chunk_bits = 0;
   };
   auto set_pass = [&](PassArgs& a, const PassInfo& p, bool with_ops) {
     a.stages = (const KStage*)DT->kstages.p + p.stage_begin;
@@ -1216,6 +1242,15 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
       tcx_status js = jit_function(P, DT, jkey, &jf);
       if (js) return js;
     }
+    int64_t Sg = S;  // CTAs per row of this launch
+    if (one && one->chunk >= 0 && (a.mode & (M_FWD | M_BWD))) {  // one exchange chunk's tiles
+      const int nc = 1 << P.xchunk_bits;
+      Sg = S / nc;
+      a.chunk_bits = P.xchunk_bits;
+      a.chunk_pos = chunk_tile_pos(P, a.wmask);
+      a.chunk_val = one->chunk;
+      a.cta_base = (int)(one->chunk * Sg);
+    }
     for (int64_t b0 = rlo; b0 < rhi; b0 += kMaxRows) {
       const int64_t rows = std::min(kMaxRows, rhi - b0);
       a.b0 = b0;
@@ -1241,20 +1276,20 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
           DT->jit_smem[jkey] = LJ.total;
         }
         void* params[] = {&a};
-        if (D.launchKernel(jf, (unsigned)S, (unsigned)rows, 1, (unsigned)(ns << a.h), 1, 1,
+        if (D.launchKernel(jf, (unsigned)Sg, (unsigned)rows, 1, (unsigned)(ns << a.h), 1, 1,
                            (unsigned)LJ.total, (CUstream)st, params, nullptr) != CUDA_SUCCESS)
           return fail(TCX_E_CUDA, "cuLaunchKernel failed for " + jit_kernel_name(jkey));
         continue;
       }
       cudaError_t e;
       if (c128)
-        e = km == 0 ? launch_f64_0(P.r, a, S, rows, L.total, st)
-                    : (km == 1 ? launch_f64_1(P.r, a, S, rows, L.total, st)
-                               : launch_f64_2(P.r, a, S, rows, L.total, st));
+        e = km == 0 ? launch_f64_0(P.r, a, Sg, rows, L.total, st)
+                    : (km == 1 ? launch_f64_1(P.r, a, Sg, rows, L.total, st)
+                               : launch_f64_2(P.r, a, Sg, rows, L.total, st));
       else
-        e = km == 0 ? launch_f32_0(P.r, a, S, rows, L.total, st)
-                    : (km == 1 ? launch_f32_1(P.r, a, S, rows, L.total, st)
-                               : launch_f32_2(P.r, a, S, rows, L.total, st));
+        e = km == 0 ? launch_f32_0(P.r, a, Sg, rows, L.total, st)
+                    : (km == 1 ? launch_f32_1(P.r, a, Sg, rows, L.total, st)
+                               : launch_f32_2(P.r, a, Sg, rows, L.total, st));
       if (e != cudaSuccess) return fail(TCX_E_CUDA, std::string("pass launch: ") + cudaGetErrorString(e));
     }
     return TCX_OK;
@@ -1285,10 +1320,11 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
       const int m = a.mode;
       const double touches = ((m & M_LOAD_PSI) ? 1 : 0) + ((m & M_STORE_PSI) ? 1 : 0) +
                              ((m & M_LOAD_LAM) ? 1 : 0) + ((m & M_STORE_LAM) ? 1 : 0);
+      const double part = (one && one->chunk >= 0) ? 1.0 / (double)(1 << P.xchunk_bits) : 1.0;
       pe.phase = phase;
       pe.index = index;
-      pe.flops = Bf * Nf * flops_amp;
-      pe.bytes = Bf * Nf * csz * touches;
+      pe.flops = Bf * Nf * flops_amp * part;
+      pe.bytes = Bf * Nf * csz * touches * part;
       g_prof.log.push_back(pe);
     }
     return TCX_OK;
@@ -1560,22 +1596,31 @@ tcx_status tcx_circuit_build(int32_t n_qubits, int32_t n_params, const tcx_gate*
     // qubits there (the rest keep paper order below them) and keep the plan with the fewest
     // segments (exchanges), then the fewest passes.  HEA: the run at the far end of the
     // CNOT ladder lets the light cone sweep a whole band of layers per segment.
+    // Each layout is planned twice: with and without keeping the exchange chunk bits out of
+    // the first window after an exchange (which lets that pass start on chunk c while the
+    // other chunks are still moving, comm.cuh); the winner has the fewest segments, then the
+    // fewest passes, then the most exchanges that overlap the next pass.
     const int n = n_qubits, g = c->plan.gbits, nl = n - g;
     std::vector<int> cands;
-    for (int b = g; b + g <= n; ++b) cands.push_back(b);
+    for (int b = g; b + g <= n; ++b) {
+      cands.push_back(b);
+      if (!c->plan.cluster) cands.push_back(-b);  // negative: with the chunk-bit constraint
+    }
     std::vector<tcx_circuit*> built(cands.size(), nullptr);
     std::atomic<int> next{0};
     auto work = [&] {
       for (int i = next++; i < (int)cands.size(); i = next++) {
         tcx_circuit* t = new (std::nothrow) tcx_circuit();
         if (!t) continue;
+        const int b0 = std::abs(cands[i]);
         std::vector<int> pos(n);
         for (int q = 0; q < g; ++q) pos[q] = n - 1 - q;                  // global: top bits
-        for (int j = 0; j < g; ++j) pos[cands[i] + j] = nl - 1 - j;      // top local bits
+        for (int j = 0; j < g; ++j) pos[b0 + j] = nl - 1 - j;            // top local bits
         int bit = nl - g - 1;
         for (int q = g; q < n; ++q)
-          if (q < cands[i] || q >= cands[i] + g) pos[q] = bit--;
+          if (q < b0 || q >= b0 + g) pos[q] = bit--;
         t->plan.init_pos = pos;
+        t->plan.xchunk_forbid = cands[i] < 0;
         std::string e2;
         tcx_status s2;
         try {
@@ -1596,10 +1641,20 @@ tcx_status tcx_circuit_build(int32_t n_qubits, int32_t n_params, const tcx_gate*
     std::vector<std::thread> th;
     for (int i = 0; i < nth; ++i) th.emplace_back(work);
     for (auto& x : th) x.join();
+    auto overlapped = [](const Plan& Q) {  // exchanges whose next pass can run by chunks
+      int k = 0;
+      for (size_t p = 1; p < Q.passes.size(); ++p)
+        if (Q.passes[p].seg != Q.passes[p - 1].seg)
+          k += pass_chunkable(Q, Q.passes[p]) + pass_chunkable(Q, Q.passes[p - 1]);
+      return k;
+    };
     for (auto*& t : built) {
       if (!t) continue;
       const Plan &A = t->plan, &Bp = c->plan;
-      if (A.nseg < Bp.nseg || (A.nseg == Bp.nseg && A.passes.size() < Bp.passes.size())) std::swap(c, t);
+      if (A.nseg < Bp.nseg ||
+          (A.nseg == Bp.nseg && (A.passes.size() < Bp.passes.size() ||
+                                 (A.passes.size() == Bp.passes.size() && overlapped(A) > overlapped(Bp)))))
+        std::swap(c, t);
       delete t;
       t = nullptr;
     }
@@ -1875,6 +1930,9 @@ tcx_status tcx_circuit_info(const tcx_circuit* circ, const tcx_pauli* pauli, tcx
   o->dense_blocks = (int)P.dblocks.size();
   o->init_h = __builtin_popcountll(P.init_hmask);
   o->cluster_bits = P.cluster ? P.gbits : 0;
+  for (size_t p = 1; p < P.passes.size(); ++p)
+    if (P.passes[p].seg != P.passes[p - 1].seg)
+      o->exchange_overlaps += pass_chunkable(P, P.passes[p]) + pass_chunkable(P, P.passes[p - 1]);
   if (!P.dblocks.empty()) {  // the trailing E / lambda pass has no gates: no backward launch
     int nb = 0;
     for (auto& p : P.passes) nb += p.ops.empty() ? 0 : 1;

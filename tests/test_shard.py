@@ -70,6 +70,7 @@ def test_sharded_layout_search_cfg5():
         C, P = tcx.Circuit(c, "c64", global_bits=g), tcx.Pauli(H)
         info = C.info(P)
         assert info["segments"] == 3 and info["fwd_passes"] <= 12, info
+        assert info["exchange_overlaps"] >= 2, info
         assert exchange_counts(C, P) == (2, 4)
         assert exchange_counts(C, P, want_grad=False)[1] == 0
 
@@ -201,3 +202,26 @@ def test_nccl_comm_world1():
     assert torch.equal(E, E0) and torch.equal(G, G0)
     with pytest.raises(tcx.TcxError):  # world 1 cannot run a 2-rank plan
         tcx.grad_sharded(tcx.Circuit(c, "c64", global_bits=1), P, comm, th)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,d,g", [(12, 3, 1), (13, 2, 2)])
+def test_sharded_exchange_overlap(n, d, g, monkeypatch):
+    """Exchanges whose next pass leaves the chunk bits out run chunk by chunk: the pass starts
+    on chunk q once chunk q has landed (comm.cuh).  Same results as the unoverlapped exchange
+    (to rounding: the chunked launch groups tiles into CTAs differently) and the oracle."""
+    from helpers import check_E, check_grad
+    from oracle import oracle as orc
+    from paper_2205_10091_b200.shard import ShardedState
+    c, H = W.hea(n, d), W.tfim_zz_x(n)
+    th = W.thetas(3, c.n_params, 300 + n)
+    S = ShardedState(c, H, "c64", g, tile_bits=8)
+    assert S.C.info(S.Pl)["exchange_overlaps"] > 0
+    E1, G1 = S.run(torch.as_tensor(th).cuda())
+    monkeypatch.setenv("TCX_XCHG_NO_OVERLAP", "1")
+    E2, G2 = S.run(torch.as_tensor(th).cuda())
+    Er, Gr = orc.value_grad_batch(c, H, th)
+    for E, G in ((E1, G1), (E2, G2)):
+        check_E(E.cpu().numpy(), Er, H, "c64")
+        check_grad(G.cpu().numpy(), Gr, H, c, "c64")
+    check_E(E1.cpu().numpy(), E2.cpu().numpy(), H, "c64")
