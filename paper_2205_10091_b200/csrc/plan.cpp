@@ -186,6 +186,65 @@ void normalize_diag(Op& op) {
   op.has_param = !par.empty();
 }
 
+// Regroup the diagonal ops of one pass (program-ordered op list).  Lowering emits a fused
+// 1-qubit op when the next multi-qubit gate reaches its qubit, so a QAOA cost layer arrives
+// interleaved with the previous mixer's rotations (U q1, U q2, D e1, U q3, D e2, ...) and
+// every term would become a phase multiply of its own.  Diagonal ops commute with each other
+// and with every op on other bits, so each may sit anywhere in the gap interval between the
+// last earlier and the first later non-diagonal op of the pass touching its bits.  The
+// non-diagonal ops keep their order; the diagonal ops of one weight class (param, |w|) are
+// placed by greedy interval stabbing (fewest gaps = fewest LUT ops after the merge below).
+void regroup_diag(const Plan& P, std::vector<int>& ops) {
+  std::vector<int> nd;                 // non-diagonal ops, in order
+  struct DI { int op, lo, hi, orig; std::pair<int, double> key; };
+  std::vector<DI> di;
+  for (int i : ops) {
+    const Op& o = P.ops[i];
+    if (o.type != OP_DIAG) { nd.push_back(i); continue; }
+    DI d{i, 0, 0, (int)nd.size(), {-2, (double)i}};
+    bool one = !o.terms.empty();
+    for (auto& tm : o.terms)
+      one = one && tm.param == o.terms[0].param && std::fabs(tm.w) == std::fabs(o.terms[0].w);
+    if (one) d.key = {o.terms[0].param, std::fabs(o.terms[0].w)};
+    di.push_back(d);
+  }
+  if (di.size() < 2) return;
+  const int m = (int)nd.size();
+  for (auto& d : di) {
+    const uint64_t b = P.ops[d.op].bits;
+    d.lo = 0;
+    for (int k = d.orig - 1; k >= 0; --k)
+      if (P.ops[nd[k]].bits & b) { d.lo = k + 1; break; }
+    d.hi = m;
+    for (int k = d.orig; k < m; ++k)
+      if (P.ops[nd[k]].bits & b) { d.hi = k; break; }
+  }
+  std::map<std::pair<int, double>, std::vector<int>> bykey;
+  for (int i = 0; i < (int)di.size(); ++i) bykey[di[i].key].push_back(i);
+  std::vector<int> gap(di.size(), -1);
+  for (auto& kv : bykey) {
+    std::vector<int> v = kv.second;
+    std::sort(v.begin(), v.end(), [&](int a, int b) {
+      return di[a].hi < di[b].hi || (di[a].hi == di[b].hi && a < b);
+    });
+    for (int a : v) {
+      if (gap[a] >= 0) continue;
+      const int pt = di[a].hi;
+      for (int b2 : v)
+        if (gap[b2] < 0 && di[b2].lo <= pt && di[b2].hi >= pt) gap[b2] = pt;
+    }
+  }
+  std::vector<std::vector<int>> at(m + 1);
+  for (int i = 0; i < (int)di.size(); ++i) at[gap[i]].push_back(di[i].op);  // original order kept
+  std::vector<int> out;
+  out.reserve(ops.size());
+  for (int g = 0; g <= m; ++g) {
+    for (int i : at[g]) out.push_back(i);
+    if (g < m) out.push_back(nd[g]);
+  }
+  ops.swap(out);
+}
+
 // Structured 2x2 class of a fused 1-qubit run (KOp.nterm of a U1 op; the JIT skips the
 // identically-zero coefficients and, in the adjoint, the R' entries the generator never
 // reads).  Each class is closed under products:
@@ -230,9 +289,28 @@ double op_weight(const Op& o) {
 // coefficient pairs (forward and adjoint forms) so the FFMA2 operands
 // load straight into aligned register pairs; complex128 stores the plain 8 Reals.
 thread_local bool g_packed_u1 = false;
+// Deferred-factor rotations (DESIGN.md §Kernels "Deferred rotation factors"): a fused run of
+// RX gates only (XT, u00 = u11 real) or RY gates only (RE, u00 = u11 real) is applied as
+// U = u00 (I + K), K off-diagonal; the kernels apply I + K (one FFMA2 per output amplitude
+// instead of an FMUL2 + FFMA2) and multiply the pass's product of the u00 back at its end.
+// Runs folded into the product initial state keep the plain form.  TCX_NO_TAN=1 turns it off.
+thread_local bool g_tan_on = false;
+int tan_kind_of(const Op& o) {
+  if (!g_tan_on || o.type != OP_U1 || o.fold_init || o.cons.empty()) return 0;
+  bool rx = true, ry = true, any = false;
+  for (auto& c : o.cons) {
+    if (c.kind == TCX_I) continue;
+    any = true;
+    rx = rx && c.kind == TCX_RX;
+    ry = ry && c.kind == TCX_RY;
+  }
+  return !any ? 0 : (rx ? 1 : (ry ? 2 : 0));
+}
 int op_mats(const Op& o) {
   switch (o.type) {
-    case OP_U1: return g_packed_u1 ? 32 : 8;
+    // complex128 deferred-factor ops append [k0, k1, exact flag, pad]; complex64 ops keep
+    // them in adjoint-half coefficient pairs the structured class never reads (materialize_kernel)
+    case OP_U1: return g_packed_u1 ? 32 : (tan_kind_of(o) ? 12 : 8);
     case OP_U2F: return 32;
     case OP_CX: return 0;
     default: return 2 * ((int)o.terms.size() + (o.lut ? 1 : 0));
@@ -1069,6 +1147,7 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
 
   // ---- pass scheduling
   g_packed_u1 = dtype == TCX_C64;
+  g_tan_on = getenv("TCX_NO_TAN") == nullptr;
   g_q_grad = P.q_grad && P.dense_k == 0;
   Scheduler S(P);
   S.lookahead = gb == 0 && P.ops.size() <= 4096 && !(getenv("TCX_PLAN_GREEDY"));
@@ -1134,6 +1213,9 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
     P.passes.push_back(std::move(pi));
   }
   static const bool lut_off = getenv("TCX_DIAG_NOLUT") != nullptr;
+  static const bool regroup_off = getenv("TCX_NO_DIAG_REGROUP") != nullptr;
+  for (auto& pass : P.passes)
+    if (!regroup_off) regroup_diag(P, pass.ops);
   // merge runs of consecutive diagonal ops within each pass (they commute, and no op of
   // the pass sits between them; ops of other passes keep their order relative to the pass)
   for (auto& pass : P.passes) {
@@ -1203,6 +1285,17 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
       }
     }
     pass.ops = out;
+    if (const char* dbg = getenv("TCX_PLAN_DEBUG"))
+      if (dbg[0] == '3') {
+        fprintf(stderr, "pass-list %d:", (int)(&pass - &P.passes[0]));
+        for (int oi : pass.ops) {
+          const Op& o = P.ops[oi];
+          if (o.type == OP_U1) fprintf(stderr, " U%d", o.b0);
+          else if (o.type == OP_DIAG) fprintf(stderr, " D%s%zu", o.lut ? "L" : "", o.terms.size());
+          else fprintf(stderr, " O");
+        }
+        fprintf(stderr, "\n");
+      }
   }
   if (P.passes.empty() || P.passes.back().seg != seg) {  // init / trailing-layout pass
     PassInfo pi;
@@ -1236,6 +1329,13 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
     for (int l = 0; l < t; ++l) loc[pass.W[l]] = l;
     int pass_acc = 0;
     uint32_t prevR = 0xFFFFFFFFu;
+    // deferred-factor ops in this pass: header [S_fwd, S_bwd] at the start of its table
+    pass.tan_hdr = -1;
+    for (auto& st : stages)
+      for (int oi : st.ops)
+        if (tan_kind_of(P.ops[oi]) && pass.tan_hdr < 0) pass.tan_hdr = 0;
+    if (pass.tan_hdr == 0) mat += 2;
+    std::vector<int> pass_kops_ops;  // plan op index of each kop of this pass (scan program)
     for (auto& st : stages) {
       KStage ks;
       std::memset(&ks, 0, sizeof(ks));
@@ -1273,6 +1373,9 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
         touched_exec |= o.bits;
         ko.acc = -1;
         ko.term = -1;
+        pass_kops_ops.push_back(oi);
+        o.tan = tan_kind_of(o);
+        o.tan_idx = o.tan ? P.ntan++ : -1;
         o.mat_off = mat;
         o.mat_len = op_mats(o);
         ko.mat = (int16_t)(mat - pass.mat_begin);
@@ -1280,7 +1383,8 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
           ko.a = (uint8_t)slot_of(o.b0);
           ko.nterm = (int16_t)u1_class_of(o.cons);
           ko.cbit = o.skip_udag ? 1 : 0;  // U1 / DIAG: backward skips U^dagger
-          ko.b = o.fold_init ? 1 : 0;      // U1: folded into the first pass's initial state
+          ko.b = (uint8_t)((o.fold_init ? 1 : 0) |  // U1: folded into the first pass's initial state
+                           (o.tan << 1));           //     deferred-factor rotation kind
         } else if (o.type == OP_U2F) {  // tile-local positions (shared-memory op)
           ko.a = (uint8_t)loc[o.b0];
           ko.b = (uint8_t)loc[o.b1];
@@ -1363,6 +1467,39 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
       P.kstages.push_back(ks);
     }
     pass.stage_count = (int)P.kstages.size() - pass.stage_begin;
+    if (pass.tan_hdr >= 0) {  // scan program: forward factors, backward walk (reverse order)
+      const bool c128p = !g_packed_u1;
+      auto flag_of = [&](const Op& o) { return o.mat_off + (c128p ? 10 : 30); };
+      SPass sp{};
+      sp.hdr = pass.mat_begin + pass.tan_hdr;
+      sp.fbeg = (int)P.sfwd.size();
+      for (int oi : pass_kops_ops)
+        if (P.ops[oi].tan) P.sfwd.push_back(SFwd{P.ops[oi].tan_idx, flag_of(P.ops[oi])});
+      sp.fcnt = (int)P.sfwd.size() - sp.fbeg;
+      sp.bbeg = (int)P.sbwd.size();
+      for (int k = (int)pass_kops_ops.size() - 1; k >= 0; --k) {
+        const Op& o = P.ops[pass_kops_ops[k]];
+        if (o.acc_off >= 0 && o.acc_len > 0 && o.pass >= 0) P.sbwd.push_back(SBwd{0, o.acc_off, o.acc_len, 0});
+        if (o.tan && !o.skip_udag) P.sbwd.push_back(SBwd{1, o.tan_idx, flag_of(o), 0});
+      }
+      sp.bcnt = (int)P.sbwd.size() - sp.bbeg;
+      P.spass.push_back(sp);
+    }
+    if (const char* dbg = getenv("TCX_PLAN_DEBUG"))
+      if (dbg[0] == '2') {  // stage-level op listing: U1 q / X t.c / D(nterms)
+        fprintf(stderr, "pass %d:", (int)(&pass - &P.passes[0]));
+        for (auto& st : stages) {
+          fprintf(stderr, " |");
+          for (int oi : st.ops) {
+            const Op& o = P.ops[oi];
+            if (o.type == OP_U1) fprintf(stderr, " U%d", o.b0);
+            else if (o.type == OP_CX) fprintf(stderr, " X%d.%d", o.b0, o.b1);
+            else if (o.type == OP_DIAG) fprintf(stderr, " D%s%zu", o.lut ? "L" : "", o.terms.size());
+            else fprintf(stderr, " F");
+          }
+        }
+        fprintf(stderr, "\n");
+      }
     {
       const KStage& ls = P.kstages.back();
       bool top = true;
@@ -1390,6 +1527,8 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
       mi.cons_begin = (int)P.dcons.size();
       mi.cons_count = (int)o.cons.size();
       mi.param = -1;
+      mi.tan = o.pass >= 0 ? o.tan : 0;
+      mi.tan_idx = o.pass >= 0 ? o.tan_idx : -1;
       for (auto& cn : o.cons) {
         DCons d{};
         d.kind = cn.kind;

@@ -55,6 +55,9 @@ struct Op {
                            // product state it produces (column 0 of its 2x2 per theta row)
   bool skip_udag = false;  // backward: no op executed before it touches its bits, so U^dagger
                            // on psi and lambda can be skipped (plan.cpp, stage emission)
+  int tan = 0;       // U1 rotation run applied as u00 (I + K) (1: RX only, 2: RY only), the
+                     // real factor u00 deferred to the pass end (plan.cpp tan_kind_of)
+  int tan_idx = -1;  // index of its u00 in the per-row fp64 factor table
   bool lut = false;  // DIAG: one weight class (param, |w|); phase from a (T+1)-entry table
   int ngroups = 0;   // DIAG (not LUT): distinct register-slot masks of its terms = complex
                      // multiplies per amplitude in the kernels (cost model)
@@ -73,6 +76,21 @@ struct MItem {
   int64_t payload;
   int32_t param, pad;
   double w;
+  int32_t tan, tan_idx;  // U1: deferred-factor rotation (Op::tan) and its factor-table index
+};
+// Deferred rotation factors (Op::tan): per pass, the forward list of factor ops (execution
+// order) and the backward walk (reverse execution order) that the scan kernel (tcx.cu) runs
+// per theta row to choose fast/exact per op, write the pass-end scales into the pass header
+// and the gradient-slot corrections S^2.
+struct SPass {
+  int32_t hdr;             // absolute offset (Reals) of the pass header [S_fwd, S_bwd]
+  int32_t fbeg, fcnt, bbeg, bcnt, pad;
+};
+struct SFwd {
+  int32_t idx, flag;       // factor index, absolute offset (Reals) of the op's exact flag
+};
+struct SBwd {
+  int32_t kind, a, b, pad; // 0: gradient slots [a, a + b); 1: factor a (flag at b)
 };
 struct DCons {       // device copy of Constituent
   int32_t kind, param;
@@ -123,6 +141,7 @@ struct PassInfo {
   int acc_begin = 0, acc_count = 0;
   int max_stage_acc = 0;
   int last_is_top = 1;   // last stage uses the load/store mapping
+  int tan_hdr = -1;      // >= 0: pass-relative offset of [S_fwd, S_bwd] (deferred factors)
 };
 
 struct Pauli {
@@ -181,6 +200,10 @@ struct Plan {
   std::vector<KTerm> kterms;
   std::vector<KStage> kstages;
   std::vector<MItem> mitems;
+  int ntan = 0;                  // deferred-factor rotation ops (Op::tan)
+  std::vector<SPass> spass;      // scan program (tan_scan_kernel), empty if ntan == 0
+  std::vector<SFwd> sfwd;
+  std::vector<SBwd> sbwd;
   std::vector<DCons> dcons;
   std::vector<GItem> gitems;
   std::vector<int32_t> param_ptr, param_list;  // CSR param -> contrib indices

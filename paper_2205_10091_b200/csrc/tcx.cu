@@ -122,6 +122,8 @@ struct MatArgs {
   int P;
   void* mats;
   int mat_total;
+  double* tanc;  // [B][ntan] u00 of deferred-factor rotations (fp64), or null
+  int ntan;
 };
 
 template <typename Real>
@@ -157,6 +159,39 @@ __global__ void materialize_kernel(const MatArgs a) {
         out[it.mat_off + 16 + 2 * i + 1] = (Real)((i & 1) ? -d : d);
       }
     }
+    if (it.tan) {
+      // deferred-factor rotation U = al (I + K): al = u00 = u11 (real for RX / RY runs),
+      // K = off-diagonal / al.  XT (RX): K01 = K10 = i tau; RE (RY): K01 = rho, K10 = rho'.
+      // The exact flag starts at 1 (plain form); tan_scan_kernel clears it when the row's
+      // growth bound allows the I + K form.
+      const double al = 0.5 * (M[0].x + M[3].x);
+      a.tanc[b * a.ntan + it.tan_idx] = al;
+      const double ia = al != 0.0 ? 1.0 / al : 0.0;
+      double k0, k1;  // XT: tau = Im u01 / al (= Im u10 / al); RE: rho = u01 / al, rho' = u10 / al
+      if (it.tan == 1) {
+        k0 = k1 = 0.5 * (M[1].y + M[2].y) * ia;
+      } else {
+        k0 = M[1].x * ia;
+        k1 = M[2].x * ia;
+      }
+      Real* o = out + it.mat_off;
+      if (sizeof(Real) == 8) {
+        o[8] = (Real)k0;
+        o[9] = (Real)k1;
+        o[10] = (Real)1;
+        o[11] = (Real)0;
+      } else if (it.tan == 1) {
+        // packed pairs the XT class never reads (adjoint half, so the generic interpreter's
+        // reads of pairs 0..7 are untouched): fwd (-tau, tau) pair 10, adjoint (tau, -tau) pair 12
+        o[20] = (Real)-k0; o[21] = (Real)k0;
+        o[24] = (Real)k0; o[25] = (Real)-k0;
+        o[30] = (Real)1; o[31] = (Real)0;  // exact flag: pair 15
+      } else {  // RE: (rho, rho) pair 9, (rho', rho') pair 11, exact flag pair 15
+        o[18] = o[19] = (Real)k0;
+        o[22] = o[23] = (Real)k1;
+        o[30] = (Real)1; o[31] = (Real)0;
+      }
+    }
   } else if (it.type == OP_U2F) {
     for (int k = 0; k < 32; ++k) out[it.mat_off + k] = (Real)a.fixed[2 * it.payload + k];
   } else {
@@ -165,6 +200,63 @@ __global__ void materialize_kernel(const MatArgs a) {
     sincos(w, &s, &c);
     out[it.mat_off] = (Real)c;
     out[it.mat_off + 1] = (Real)s;
+  }
+}
+
+// Deferred rotation factors (plan.cpp tan_kind_of): per theta row and
+// pass, walk the pass's factor ops in execution order and keep the I + K form for an op while
+// the product of the |u00| applied so far stays >= 2^-40 (kernel values are the true state
+// over that product, so they and the FP32 products of two of them stay finite); the others
+// keep their exact flag and the plain form.  Writes the pass header [S_fwd, S_bwd] (the
+// factors the forward / backward ops of the pass leave to its end) and, for the backward
+// walk in reverse execution order, the correction S^2 of every gradient slot (its psi and
+// lambda both carry the factors of the U^dagger applied before it in the pass).
+struct ScanArgs {
+  const SPass* sp;
+  int npass;
+  const SFwd* fw;
+  const SBwd* bw;
+  const double* tanc;
+  int ntan;
+  void* mats;
+  int mat_total;
+  double* corr;  // [B][acc_total] or null
+  int acc_total;
+  int64_t b0;
+};
+template <typename Real>
+__global__ void tan_scan_kernel(const ScanArgs a) {
+  const int64_t b = a.b0 + blockIdx.x;
+  Real* m = reinterpret_cast<Real*>(a.mats) + b * a.mat_total;
+  const double* tc = a.tanc + b * a.ntan;
+  double* corr = a.corr ? a.corr + b * a.acc_total : nullptr;
+  if (corr)
+    for (int k = threadIdx.x; k < a.acc_total; k += blockDim.x) corr[k] = 1.0;
+  __syncthreads();
+  for (int p = threadIdx.x; p < a.npass; p += blockDim.x) {
+    const SPass sp = a.sp[p];
+    double prod = 1.0, S = 1.0;
+    for (int i = 0; i < sp.fcnt; ++i) {
+      const SFwd f = a.fw[sp.fbeg + i];
+      const double al = tc[f.idx];
+      if (fabs(al) > 0.0 && prod * fabs(al) >= 0x1p-40) {
+        prod *= fabs(al);
+        S *= al;
+        m[f.flag] = (Real)0;
+      }
+    }
+    m[sp.hdr] = (Real)S;
+    double Sb = 1.0;
+    for (int i = 0; i < sp.bcnt; ++i) {
+      const SBwd w = a.bw[sp.bbeg + i];
+      if (w.kind == 0) {
+        if (corr)
+          for (int k = 0; k < w.b; ++k) corr[w.a + k] = Sb * Sb;
+      } else if (m[w.b] == (Real)0) {
+        Sb *= tc[w.a];
+      }
+    }
+    m[sp.hdr + 1] = (Real)Sb;
   }
 }
 
@@ -187,6 +279,7 @@ struct FinArgs {
   double* E;
   double* grad;         // may be null
   int64_t b0;
+  const double* corr;   // [B][K] deferred-factor corrections of the slot sums, or null
 };
 
 // Deterministic fixed-order fp64 reductions (C10) and the gradient
@@ -218,7 +311,7 @@ __global__ void finalize_kernel(const FinArgs a) {
     double s = 0.0;
     const double* src = a.part + b * (int64_t)a.S * a.K + k;
     for (int sl = 0; sl < a.S; ++sl) s += src[(int64_t)sl * a.K];
-    tot[k] = s;
+    tot[k] = a.corr ? s * a.corr[b * a.K + k] : s;
   }
   __syncthreads();
   double* ctb = a.contrib + b * a.ncontrib;
@@ -320,6 +413,7 @@ namespace tcx {
 struct DeviceTables {
   DevBuf kops, kterms, kstages, mitems, dcons, gitems, pptr, plist, fixed, layout, swb;
   DevBuf dblocks, dgates, dpblocks;  // dense k-qubit blocks (dense.cuh)
+  DevBuf spass, sfwd, sbwd;          // deferred-factor scan program (tan_scan_kernel)
   DevBuf cut[15];                    // LUT cut tables (Plan::cut_sets), 2^nloc bytes each
   std::map<std::string, CUfunction> jit;   // key (jit.h)
   std::map<std::string, size_t> jit_smem;  // dynamic smem opted in per function
@@ -443,7 +537,8 @@ tcx_status device_tables(Plan& P, DeviceTables*& out) {
       (s = upload(T->kstages, P.kstages)) || (s = upload(T->mitems, P.mitems)) ||
       (s = upload(T->dcons, P.dcons)) || (s = upload(T->gitems, P.gitems)) ||
       (s = upload(T->pptr, P.param_ptr)) || (s = upload(T->plist, P.param_list)) ||
-      (s = upload(T->fixed, P.fixed)))
+      (s = upload(T->fixed, P.fixed)) || (s = upload(T->spass, P.spass)) ||
+      (s = upload(T->sfwd, P.sfwd)) || (s = upload(T->sbwd, P.sbwd)))
     return s;
   std::vector<int> lay(P.layout, P.layout + P.n);
   if ((s = upload(T->layout, lay))) return s;
@@ -676,6 +771,7 @@ enum { K_EXPECT = 0, K_GRAD = 1, K_STATE = 2 };
 
 struct WsLayout {
   size_t psi, lam, mats, part, epart, tot, contrib, theta, E, grad, total;
+  size_t tanc, corr;  // deferred-factor rotations: u00 per row, slot corrections (0: none)
   size_t dmats, dshared, dpart, drs, dq;  // dense blocks: U tables, R' partials / sums, q
   bool mega;
 };
@@ -716,6 +812,8 @@ WsLayout ws_layout(const Plan& P, const Binding* Bd, int64_t B, int kind, bool h
   w.epart = kind != K_STATE ? take(B * S * EU * 8) : 0;
   w.tot = kind == K_GRAD ? take(B * std::max(P.acc_total, 1) * 8) : 0;
   w.contrib = kind == K_GRAD ? take(B * std::max(P.n_contrib, 1) * 8) : 0;
+  w.tanc = P.ntan > 0 ? take(B * P.ntan * 8) : 0;
+  w.corr = P.ntan > 0 && kind == K_GRAD ? take(B * std::max(P.acc_total, 1) * 8) : 0;
   if (!P.dblocks.empty()) {
     w.dmats = take(B * std::max(P.dmat_row, 1) * 2 * rs);
     w.dshared = take(std::max(P.dmat_shared, 1) * 2 * rs);
@@ -879,6 +977,31 @@ int chunk_tile_pos(const Plan& P, uint64_t wmask) {
   return k;
 }
 
+// deferred-factor scan after materialize (JIT plans only: the generic interpreter applies the
+// plain coefficients and never reads the flags or pass headers)
+tcx_status tan_scan(const Plan& P, DeviceTables* DT, char* W, const WsLayout& wl, int64_t b0,
+                    int64_t rows, bool c128, cudaStream_t st) {
+  if (P.ntan == 0 || !P.jit_on || P.spass.empty()) return TCX_OK;
+  ScanArgs sa;
+  sa.sp = (const SPass*)DT->spass.p;
+  sa.npass = (int)P.spass.size();
+  sa.fw = (const SFwd*)DT->sfwd.p;
+  sa.bw = (const SBwd*)DT->sbwd.p;
+  sa.tanc = (const double*)(W + wl.tanc);
+  sa.ntan = P.ntan;
+  sa.mats = W + wl.mats;
+  sa.mat_total = P.mat_total;
+  sa.corr = wl.corr ? (double*)(W + wl.corr) : nullptr;
+  sa.acc_total = std::max(P.acc_total, 1);
+  sa.b0 = b0;
+  if (c128)
+    tan_scan_kernel<double><<<(unsigned)rows, 64, 0, st>>>(sa);
+  else
+    tan_scan_kernel<float><<<(unsigned)rows, 64, 0, st>>>(sa);
+  CUDA_TRY(cudaGetLastError());
+  return TCX_OK;
+}
+
 // Cluster-resident plans (tcx_build_opts.cluster_bits): materialise the per-
 // theta matrices, one megakernel launch with a cluster of G = 2^g CTAs per theta row
 // (jit.cpp cluster_kernel: psi and lambda stay in registers, exchanges through distributed
@@ -952,12 +1075,15 @@ tcx_status run_cluster(Plan& P, const tcx_pauli* H, const double* theta, int64_t
     ma.P = P.P;
     ma.mats = W + wl.mats + b0 * P.mat_total * rs;
     ma.mat_total = P.mat_total;
+    ma.tanc = P.ntan > 0 ? (double*)(W + wl.tanc) + b0 * P.ntan : nullptr;
+    ma.ntan = P.ntan;
     dim3 g((ma.nitems + 127) / 128, (unsigned)rows);
     if (c128)
       materialize_kernel<double><<<g, 128, 0, st>>>(ma);
     else
       materialize_kernel<float><<<g, 128, 0, st>>>(ma);
     CUDA_TRY(cudaGetLastError());
+    if ((s = tan_scan(P, DT, W, wl, b0, rows, c128, st))) return s;
   }
   // ---- the megakernel: rows in chunks (grid.x = rows * G < 2^31)
   PassArgs a;
@@ -1043,6 +1169,7 @@ tcx_status run_cluster(Plan& P, const tcx_pauli* H, const double* theta, int64_t
     f.E = E;
     f.grad = kind == K_GRAD && P.P > 0 ? grad : nullptr;
     f.b0 = b0;
+    f.corr = wl.corr && P.jit_on ? (const double*)(W + wl.corr) : nullptr;
     finalize_kernel<<<(unsigned)rows, 256, 0, st>>>(f);
     CUDA_TRY(cudaGetLastError());
   }
@@ -1110,12 +1237,15 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
     ma.P = P.P;
     ma.mats = W + wl.mats + b0 * P.mat_total * rs;
     ma.mat_total = P.mat_total;
+    ma.tanc = P.ntan > 0 ? (double*)(W + wl.tanc) + b0 * P.ntan : nullptr;
+    ma.ntan = P.ntan;
     dim3 g((ma.nitems + 127) / 128, (unsigned)rows);
     if (c128)
       materialize_kernel<double><<<g, 128, 0, st>>>(ma);
     else
       materialize_kernel<float><<<g, 128, 0, st>>>(ma);
     CUDA_TRY(cudaGetLastError());
+    if ((s = tan_scan(P, DT, W, wl, b0, rows, c128, st))) return s;
   }
   // ---- input states (PAPER.md:1005-1044 inputs): the first pass / block reads them
   if (psi0) {
@@ -1533,6 +1663,7 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
       f.E = E;
       f.grad = kind == K_GRAD && P.P > 0 ? grad : nullptr;
       f.b0 = b0;
+      f.corr = wl.corr && P.jit_on ? (const double*)(W + wl.corr) : nullptr;
       finalize_kernel<<<(unsigned)rows, 256, 0, st>>>(f);
       CUDA_TRY(cudaGetLastError());
       if (f.qcontrib && P.P > 0) {  // window q_grad plans: per-parameter CSR sums
