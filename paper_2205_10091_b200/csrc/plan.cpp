@@ -1147,7 +1147,7 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
 
   // ---- pass scheduling
   g_packed_u1 = dtype == TCX_C64;
-  g_tan_on = getenv("TCX_NO_TAN") == nullptr;
+  g_tan_on = getenv("TCX_NO_TAN") == nullptr && !P.cluster;  // cluster kernels: no plain fallback
   g_q_grad = P.q_grad && P.dense_k == 0;
   Scheduler S(P);
   S.lookahead = gb == 0 && P.ops.size() <= 4096 && !(getenv("TCX_PLAN_GREEDY"));
@@ -1329,12 +1329,13 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
     for (int l = 0; l < t; ++l) loc[pass.W[l]] = l;
     int pass_acc = 0;
     uint32_t prevR = 0xFFFFFFFFu;
-    // deferred-factor ops in this pass: header [S_fwd, S_bwd] at the start of its table
+    // deferred-factor ops in this pass: header [S_fwd, S_bwd, plain, pad] at the start of its
+    // table (plain = 1: this row runs the pass's plain-form variant)
     pass.tan_hdr = -1;
     for (auto& st : stages)
       for (int oi : st.ops)
         if (tan_kind_of(P.ops[oi]) && pass.tan_hdr < 0) pass.tan_hdr = 0;
-    if (pass.tan_hdr == 0) mat += 2;
+    if (pass.tan_hdr == 0) mat += 4;
     std::vector<int> pass_kops_ops;  // plan op index of each kop of this pass (scan program)
     for (auto& st : stages) {
       KStage ks;

@@ -83,7 +83,7 @@ struct MItem {
 // per theta row to choose fast/exact per op, write the pass-end scales into the pass header
 // and the gradient-slot corrections S^2.
 struct SPass {
-  int32_t hdr;             // absolute offset (Reals) of the pass header [S_fwd, S_bwd]
+  int32_t hdr;             // absolute offset (Reals) of the pass header [S_fwd, S_bwd, plain, pad]
   int32_t fbeg, fcnt, bbeg, bcnt, pad;
 };
 struct SFwd {
@@ -141,7 +141,7 @@ struct PassInfo {
   int acc_begin = 0, acc_count = 0;
   int max_stage_acc = 0;
   int last_is_top = 1;   // last stage uses the load/store mapping
-  int tan_hdr = -1;      // >= 0: pass-relative offset of [S_fwd, S_bwd] (deferred factors)
+  int tan_hdr = -1;      // >= 0: pass-relative offset of [S_fwd, S_bwd, plain, pad] (deferred factors)
 };
 
 struct Pauli {

@@ -162,8 +162,7 @@ __global__ void materialize_kernel(const MatArgs a) {
     if (it.tan) {
       // deferred-factor rotation U = al (I + K): al = u00 = u11 (real for RX / RY runs),
       // K = off-diagonal / al.  XT (RX): K01 = K10 = i tau; RE (RY): K01 = rho, K10 = rho'.
-      // The exact flag starts at 1 (plain form); tan_scan_kernel clears it when the row's
-      // growth bound allows the I + K form.
+      // The plain coefficients above stay for rows whose pass runs the plain variant.
       const double al = 0.5 * (M[0].x + M[3].x);
       a.tanc[b * a.ntan + it.tan_idx] = al;
       const double ia = al != 0.0 ? 1.0 / al : 0.0;
@@ -178,18 +177,14 @@ __global__ void materialize_kernel(const MatArgs a) {
       if (sizeof(Real) == 8) {
         o[8] = (Real)k0;
         o[9] = (Real)k1;
-        o[10] = (Real)1;
-        o[11] = (Real)0;
       } else if (it.tan == 1) {
-        // packed pairs the XT class never reads (adjoint half, so the generic interpreter's
-        // reads of pairs 0..7 are untouched): fwd (-tau, tau) pair 10, adjoint (tau, -tau) pair 12
+        // packed pairs the XT class never reads (adjoint half, so the generic kernel's reads
+        // of pairs 0..7 are untouched): fwd (-tau, tau) pair 10, adjoint (tau, -tau) pair 12
         o[20] = (Real)-k0; o[21] = (Real)k0;
         o[24] = (Real)k0; o[25] = (Real)-k0;
-        o[30] = (Real)1; o[31] = (Real)0;  // exact flag: pair 15
-      } else {  // RE: (rho, rho) pair 9, (rho', rho') pair 11, exact flag pair 15
+      } else {  // RE: (rho, rho) pair 9, (rho', rho') pair 11
         o[18] = o[19] = (Real)k0;
         o[22] = o[23] = (Real)k1;
-        o[30] = (Real)1; o[31] = (Real)0;
       }
     }
   } else if (it.type == OP_U2F) {
@@ -204,13 +199,11 @@ __global__ void materialize_kernel(const MatArgs a) {
 }
 
 // Deferred rotation factors (plan.cpp tan_kind_of): per theta row and
-// pass, walk the pass's factor ops in execution order and keep the I + K form for an op while
-// the product of the |u00| applied so far stays >= 2^-40 (kernel values are the true state
-// over that product, so they and the FP32 products of two of them stay finite); the others
-// keep their exact flag and the plain form.  Writes the pass header [S_fwd, S_bwd] (the
-// factors the forward / backward ops of the pass leave to its end) and, for the backward
-// walk in reverse execution order, the correction S^2 of every gradient slot (its psi and
-// lambda both carry the factors of the U^dagger applied before it in the pass).
+// pass, decide whether the pass runs its I + K form or its plain form (both tile loops are in
+// the pass's JIT kernel, one uniform branch per CTA), and write the pass header [S_fwd, S_bwd, plain]
+// (the factors the forward / backward ops leave to the pass end) and, walking the backward
+// in reverse execution order, the correction S^2 of every gradient slot (its psi and lambda
+// both carry the factors of the U^dagger applied before it in the pass).
 struct ScanArgs {
   const SPass* sp;
   int npass;
@@ -235,28 +228,30 @@ __global__ void tan_scan_kernel(const ScanArgs a) {
   __syncthreads();
   for (int p = threadIdx.x; p < a.npass; p += blockDim.x) {
     const SPass sp = a.sp[p];
+    // kernel values = true state / (product of the |u00| applied so far in the pass): the
+    // I + K form is used for the whole pass while that product stays >= 2^-40, so the values,
+    // the FP32 products of two of them and their tile sums stay finite
     double prod = 1.0, S = 1.0;
     for (int i = 0; i < sp.fcnt; ++i) {
-      const SFwd f = a.fw[sp.fbeg + i];
-      const double al = tc[f.idx];
-      if (fabs(al) > 0.0 && prod * fabs(al) >= 0x1p-40) {
-        prod *= fabs(al);
-        S *= al;
-        m[f.flag] = (Real)0;
-      }
+      const double al = tc[a.fw[sp.fbeg + i].idx];
+      prod *= fabs(al);
+      S *= al;
     }
-    m[sp.hdr] = (Real)S;
+    const bool fast = prod >= 0x1p-40;
     double Sb = 1.0;
     for (int i = 0; i < sp.bcnt; ++i) {
       const SBwd w = a.bw[sp.bbeg + i];
       if (w.kind == 0) {
-        if (corr)
+        if (corr && fast)
           for (int k = 0; k < w.b; ++k) corr[w.a + k] = Sb * Sb;
-      } else if (m[w.b] == (Real)0) {
+      } else {
         Sb *= tc[w.a];
       }
     }
-    m[sp.hdr + 1] = (Real)Sb;
+    m[sp.hdr] = (Real)(fast ? S : 1.0);
+    m[sp.hdr + 1] = (Real)(fast ? Sb : 1.0);
+    m[sp.hdr + 2] = (Real)(fast ? 0 : 1);
+    m[sp.hdr + 3] = (Real)0;
   }
 }
 
@@ -1445,6 +1440,7 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
     }
     tcx_status r0 = launch_raw(a, jkey);
     if (r0) return r0;
+
     if (g_prof.on) {
       CUDA_TRY(cudaEventRecord(pe.b, st));
       const int m = a.mode;

@@ -1,6 +1,7 @@
 """GPU parity of the deferred-factor rotations: fused RX-only / RY-only
 runs applied as u00 (I + K) with the pass's product of u00 multiplied back at its end, and the
-per-row exact fallback (tan_scan_kernel) for rows whose factors would leave the FP32 range.
+per-(row, pass) plain fallback (tan_scan_kernel; the generic kernel runs those rows) for rows
+whose factors would leave the FP32 range.
 
 Checked against the CPU oracle (C9 tolerances, tests/helpers.py) and against the same plan
 built with TCX_NO_TAN=1 (plain 2x2 arithmetic)."""
@@ -109,8 +110,9 @@ def test_tan_state_and_expect(tc, dtype):
 
 
 def test_tan_all_exact_rows(tc):
-    """A pass of RX(pi) on every qubit: every factor is ~6e-17, so all but the first few ops
-    of each pass fall back to the plain form; results still match the oracle."""
+    """A pass of RX(pi) on every qubit: every factor is ~6e-17, so rows 0 and 1 run every such
+    pass on the generic kernel (plain form) while row 2 runs the JIT kernels; all match the
+    oracle."""
     n = 12
     c = W.Circuit(n, 1)
     for _ in range(3):
