@@ -54,6 +54,7 @@ bool unitary_check(const double* m, int d) {
 }
 
 // ------------------------------------------------------------------ lowering
+int tan_kind_of(const Op& o);  // deferred-factor kind (below)
 struct Lowerer {
   Plan& P;
   struct Run {
@@ -81,7 +82,21 @@ struct Lowerer {
     for (int b = 0; b < P.n; ++b)
       if (op.bits >> b & 1) last_on_bit[b] = idx;
     if (op.type == OP_DIAG) last_diag = idx;
+    const bool derive = op.type == OP_U1 && tan_kind_of(op) == 3;
+    const int bit = op.b0;
     P.ops.push_back(std::move(op));
+    if (derive) {
+      // U = |u00| Phi (I + K): the kernels apply (I + K) (scale deferred); Phi = diag(u00, u11)
+      // / |u00| = e^{i gamma} e^{i w Z} follows as this diagonal op (materialize_kernel writes
+      // gamma and w from the same fused 2x2), free to move and merge like any other
+      Op d;
+      d.type = OP_DIAG;
+      d.bits = 1ull << bit;
+      d.need = 0;
+      d.terms.push_back({0, -2 - idx, 0.0});
+      d.terms.push_back({1ull << bit, -2 - idx, 0.0});
+      emit(std::move(d));
+    }
   }
   void emit_diag(const std::vector<DiagTerm>& terms, uint64_t bits) {
     if (terms.empty()) return;
@@ -164,7 +179,9 @@ void normalize_diag(Op& op) {
   std::vector<DiagTerm> fixed, par;
   for (auto& kv : acc) {
     DiagTerm t{kv.first.second, kv.first.first, kv.second, -1};
-    if (t.param < 0) {
+    if (t.param <= -2) {
+      fixed.push_back(t);  // derived phase (kind-3 U1): its value comes from materialize
+    } else if (t.param < 0) {
       if (t.w != 0.0) fixed.push_back(t);
     } else {
       par.push_back(t);
@@ -190,34 +207,48 @@ void normalize_diag(Op& op) {
 // 1-qubit op when the next multi-qubit gate reaches its qubit, so a QAOA cost layer arrives
 // interleaved with the previous mixer's rotations (U q1, U q2, D e1, U q3, D e2, ...) and
 // every term would become a phase multiply of its own.  Diagonal ops commute with each other
-// and with every op on other bits, so each may sit anywhere in the gap interval between the
-// last earlier and the first later non-diagonal op of the pass touching its bits.  The
+// and with every op on other bits, and pass CNOTs by conjugation, so each may sink to any gap
+// before the first later U1 / U2F op of the pass touching its (conjugated) bits.  The
 // non-diagonal ops keep their order; the diagonal ops of one weight class (param, |w|) are
 // placed by greedy interval stabbing (fewest gaps = fewest LUT ops after the merge below).
-void regroup_diag(const Plan& P, std::vector<int>& ops) {
+void regroup_diag(Plan& P, std::vector<int>& ops) {
   std::vector<int> nd;                 // non-diagonal ops, in order
-  struct DI { int op, lo, hi, orig; std::pair<int, double> key; };
+  struct DI { int op, hi, orig; std::pair<int, double> key; };
   std::vector<DI> di;
   for (int i : ops) {
     const Op& o = P.ops[i];
     if (o.type != OP_DIAG) { nd.push_back(i); continue; }
-    DI d{i, 0, 0, (int)nd.size(), {-2, (double)i}};
-    bool one = !o.terms.empty();
-    for (auto& tm : o.terms)
+    DI d{i, 0, (int)nd.size(), {-3, (double)i}};
+    bool one = !o.terms.empty(), derived = !o.terms.empty();
+    for (auto& tm : o.terms) {
       one = one && tm.param == o.terms[0].param && std::fabs(tm.w) == std::fabs(o.terms[0].w);
-    if (one) d.key = {o.terms[0].param, std::fabs(o.terms[0].w)};
+      derived = derived && tm.param <= -2;
+    }
+    if (derived) d.key = {-2, 0.0};  // kind-3 phases: one class for placement
+    else if (one) d.key = {o.terms[0].param, std::fabs(o.terms[0].w)};
     di.push_back(d);
   }
-  if (di.size() < 2) return;
+  if (di.empty()) return;
   const int m = (int)nd.size();
+  // Sinking a diagonal past a CNOT conjugates it: a term on the target t picks up the control
+  // c (Z_t -> Z_c Z_t); a term on the control alone commutes.  Only U1 / U2F ops on a term's
+  // bits stop it.
+  auto pass_over = [&](std::vector<uint64_t>& masks, const Op& x) {
+    if (x.type == OP_CX) {
+      for (auto& mk : masks)
+        if (mk >> x.b0 & 1) mk ^= 1ull << x.b1;
+      return true;
+    }
+    uint64_t u = 0;
+    for (auto mk : masks) u |= mk;
+    return (x.bits & u) == 0;
+  };
   for (auto& d : di) {
-    const uint64_t b = P.ops[d.op].bits;
-    d.lo = 0;
-    for (int k = d.orig - 1; k >= 0; --k)
-      if (P.ops[nd[k]].bits & b) { d.lo = k + 1; break; }
+    std::vector<uint64_t> masks;
+    for (auto& tm : P.ops[d.op].terms) masks.push_back(tm.mask);
     d.hi = m;
     for (int k = d.orig; k < m; ++k)
-      if (P.ops[nd[k]].bits & b) { d.hi = k; break; }
+      if (!pass_over(masks, P.ops[nd[k]])) { d.hi = k; break; }
   }
   std::map<std::pair<int, double>, std::vector<int>> bykey;
   for (int i = 0; i < (int)di.size(); ++i) bykey[di[i].key].push_back(i);
@@ -231,11 +262,22 @@ void regroup_diag(const Plan& P, std::vector<int>& ops) {
       if (gap[a] >= 0) continue;
       const int pt = di[a].hi;
       for (int b2 : v)
-        if (gap[b2] < 0 && di[b2].lo <= pt && di[b2].hi >= pt) gap[b2] = pt;
+        if (gap[b2] < 0 && di[b2].orig <= pt && di[b2].hi >= pt) gap[b2] = pt;
     }
   }
   std::vector<std::vector<int>> at(m + 1);
-  for (int i = 0; i < (int)di.size(); ++i) at[gap[i]].push_back(di[i].op);  // original order kept
+  for (int i = 0; i < (int)di.size(); ++i) {
+    Op& o = P.ops[di[i].op];
+    std::vector<uint64_t> masks;
+    for (auto& tm : o.terms) masks.push_back(tm.mask);
+    for (int k = di[i].orig; k < gap[i]; ++k) pass_over(masks, P.ops[nd[k]]);
+    o.bits = 0;
+    for (size_t t2 = 0; t2 < masks.size(); ++t2) {
+      o.terms[t2].mask = masks[t2];
+      o.bits |= masks[t2];
+    }
+    at[gap[i]].push_back(di[i].op);  // original order kept
+  }
   std::vector<int> out;
   out.reserve(ops.size());
   for (int g = 0; g <= m; ++g) {
@@ -295,22 +337,41 @@ thread_local bool g_packed_u1 = false;
 // instead of an FMUL2 + FFMA2) and multiply the pass's product of the u00 back at its end.
 // Runs folded into the product initial state keep the plain form.  TCX_NO_TAN=1 turns it off.
 thread_local bool g_tan_on = false;
+thread_local bool g_tan_general = false;  // kind 3 (TCX_TAN_GENERAL=1)
+int u1_class_of(const std::vector<Constituent>& cons);
 int tan_kind_of(const Op& o) {
   if (!g_tan_on || o.type != OP_U1 || o.fold_init || o.cons.empty()) return 0;
-  bool rx = true, ry = true, any = false;
+  bool rx = true, ry = true, any = false, unit = true;
   for (auto& c : o.cons) {
+    switch (c.kind) {  // unitary constituents only (payload U1, noise and structure gates excluded)
+      case TCX_I: case TCX_X: case TCX_Y: case TCX_Z: case TCX_H: case TCX_S: case TCX_SDG:
+      case TCX_T: case TCX_TDG: case TCX_RX: case TCX_RY: case TCX_RZ: break;
+      default: unit = false; break;
+    }
     if (c.kind == TCX_I) continue;
     any = true;
     rx = rx && c.kind == TCX_RX;
     ry = ry && c.kind == TCX_RY;
   }
-  return !any ? 0 : (rx ? 1 : (ry ? 2 : 0));
+  if (!any || !unit) return 0;
+  if (rx) return 1;
+  if (ry) return 2;
+  // general runs (the structured classes already cost 2 FFMA2 per output amplitude): opt-in,
+  // measured slower -- the derived phases merge into diagonal ops that stall the stage
+  // schedule (cfg2: 44 -> 58 register stages, 3572 -> 3490 circuits/s; cfg1 330k -> 216k)
+  return (g_tan_general && u1_class_of(o.cons) == 0) ? 3 : 0;
 }
 int op_mats(const Op& o) {
   switch (o.type) {
     // complex128 deferred-factor ops append [k0, k1, exact flag, pad]; complex64 ops keep
     // them in adjoint-half coefficient pairs the structured class never reads (materialize_kernel)
-    case OP_U1: return g_packed_u1 ? 32 : (tan_kind_of(o) ? 12 : 8);
+    // kind 3 appends the four coefficient pairs of K (forward) and K^dagger (adjoint):
+    // 8 packed pairs + 1 spare (complex64) / [k01, k10] complex (complex128)
+    case OP_U1: {
+      const int tk = tan_kind_of(o);
+      if (g_packed_u1) return tk == 3 ? 50 : 32;
+      return tk == 3 ? 14 : (tk ? 12 : 8);
+    }
     case OP_U2F: return 32;
     case OP_CX: return 0;
     default: return 2 * ((int)o.terms.size() + (o.lut ? 1 : 0));
@@ -1027,6 +1088,9 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
   for (int q = 0; q < n; ++q) pos[q] = n - 1 - q;  // PAPER.md:249 qubit 0 = MSB
   if ((int)P.init_pos.size() == n)  // sharded layout search (tcx_circuit_build)
     for (int q = 0; q < n; ++q) pos[q] = P.init_pos[q];
+  g_packed_u1 = dtype == TCX_C64;
+  g_tan_on = getenv("TCX_NO_TAN") == nullptr && !P.cluster && P.dense_k == 0;  // cluster kernels: no plain variant
+  g_tan_general = getenv("TCX_TAN_GENERAL") != nullptr;
   Lowerer L(P);
   auto payload_copy_raw = [&](int64_t off, int elems) {  // complex elements, no checks
     int64_t at = (int64_t)P.fixed.size() / 2;
@@ -1147,7 +1211,6 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
 
   // ---- pass scheduling
   g_packed_u1 = dtype == TCX_C64;
-  g_tan_on = getenv("TCX_NO_TAN") == nullptr && !P.cluster;  // cluster kernels: no plain fallback
   g_q_grad = P.q_grad && P.dense_k == 0;
   Scheduler S(P);
   S.lookahead = gb == 0 && P.ops.size() <= 4096 && !(getenv("TCX_PLAN_GREEDY"));
@@ -1552,6 +1615,7 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
         gi.cons_begin = mi.cons_begin;
         gi.cons_count = mi.cons_count;
         gi.contrib = -1;
+        gi.phase = o.tan == 3 ? 1 : 0;
         P.gitems.push_back(gi);
       }
     } else if (o.type == OP_U2F) {
@@ -1582,6 +1646,22 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
         mi.param = o.terms[i].param;
         mi.w = o.terms[i].w;
         mi.payload = -1;
+        if (mi.param <= -2) {  // derived phase of a kind-3 U1: recomputed from its constituents
+          const Op& src = P.ops[-2 - mi.param];
+          mi.cons_begin = (int)P.dcons.size();
+          mi.cons_count = (int)src.cons.size();
+          for (auto& cn : src.cons) {
+            DCons d{};
+            d.kind = cn.kind;
+            d.param = cn.param;
+            d.coeff = cn.coeff;
+            d.payload = cn.payload;
+            d.contrib = -1;
+            P.dcons.push_back(d);
+          }
+          mi.tan = 4;
+          mi.tan_idx = o.terms[i].mask ? 1 : 0;  // 0: global part gamma, 1: Z part w
+        }
         P.mitems.push_back(mi);
       }
     }

@@ -36,7 +36,8 @@ struct Constituent {
 // a = coeff*theta give w = -coeff/2.
 struct DiagTerm {
   uint64_t mask;
-  int32_t param;
+  int32_t param;      // theta column, -1 fixed, <= -2 derived: the diagonal phase Phi of the
+                      // kind-3 U1 op (-2 - param) (mask 0: its global part, else its Z part)
   double w;
   int32_t slot = -1;  // op-local gradient slot (param terms sharing (param, w))
 };
@@ -55,8 +56,9 @@ struct Op {
                            // product state it produces (column 0 of its 2x2 per theta row)
   bool skip_udag = false;  // backward: no op executed before it touches its bits, so U^dagger
                            // on psi and lambda can be skipped (plan.cpp, stage emission)
-  int tan = 0;       // U1 rotation run applied as u00 (I + K) (1: RX only, 2: RY only), the
-                     // real factor u00 deferred to the pass end (plan.cpp tan_kind_of)
+  int tan = 0;       // U1 applied as (I + K) with a deferred real factor (plan.cpp tan_kind_of):
+                     // 1 RX only, 2 RY only (u00 = u11 real), 3 general unitary run, whose
+                     // diagonal phase Phi = diag(u00, u11) / |u00| follows as a derived DIAG op
   int tan_idx = -1;  // index of its u00 in the per-row fp64 factor table
   bool lut = false;  // DIAG: one weight class (param, |w|); phase from a (T+1)-entry table
   int ngroups = 0;   // DIAG (not LUT): distinct register-slot masks of its terms = complex
@@ -105,6 +107,8 @@ struct GItem {       // finalize items
   double factor;     // DIAG: -2 * w
   int32_t contrib;
   int32_t re_acc;    // q_grad: slot of the real-part sums (U1: acc + 3), else -1
+  int32_t phase;     // U1 kind 3 (Op::tan): R' was taken before its diagonal phase, so the
+  int32_t pad;       //   generators are conjugated B' = Phi^dagger B Phi (finalize_kernel)
 };
 
 // Dense k-qubit block (north_star step 2): a run of gates fused into one

@@ -140,6 +140,20 @@ __global__ void materialize_kernel(const MatArgs a) {
       gate1(a.cons[it.cons_begin + c], th, a.fixed, G);
       mat2mul(G, M, M);
     }
+    double al3 = 0.0;
+    if (it.tan == 3) {
+      // kind 3: U = |u00| Phi (I + K), Phi = diag(u00, u11) / |u00| (applied by the derived
+      // diagonal op); the standard slots carry V = Phi^dagger U = |u00| (I + K), which the
+      // plain variant applies
+      al3 = sqrt(M[0].x * M[0].x + M[0].y * M[0].y);
+      const double r1 = sqrt(M[3].x * M[3].x + M[3].y * M[3].y);
+      const cdd e0 = al3 > 0.0 ? cdd{M[0].x / al3, -M[0].y / al3} : cdd{1, 0};  // e^{-i alpha}
+      const cdd e1 = r1 > 0.0 ? cdd{M[3].x / r1, -M[3].y / r1} : cdd{1, 0};     // e^{-i beta}
+      M[0] = cmul(e0, M[0]);
+      M[1] = cmul(e0, M[1]);
+      M[2] = cmul(e1, M[2]);
+      M[3] = cmul(e1, M[3]);
+    }
     if (sizeof(Real) == 8) {
       for (int k = 0; k < 4; ++k) {
         out[it.mat_off + 2 * k] = (Real)M[k].x;
@@ -159,7 +173,26 @@ __global__ void materialize_kernel(const MatArgs a) {
         out[it.mat_off + 16 + 2 * i + 1] = (Real)((i & 1) ? -d : d);
       }
     }
-    if (it.tan) {
+    if (it.tan == 3) {
+      // K01 = kappa = V01 / |u00|, K10 = kappa' = V10 / |u00|; forward pairs (zr, zr), (-zi, zi)
+      // for z = kappa, kappa' (reals 32..39), adjoint I + K^dagger: conj(kappa'), conj(kappa)
+      a.tanc[b * a.ntan + it.tan_idx] = al3;
+      const double ia = al3 > 0.0 ? 1.0 / al3 : 0.0;
+      const double kr = M[1].x * ia, ki = M[1].y * ia, qr = M[2].x * ia, qi = M[2].y * ia;
+      Real* o = out + it.mat_off;
+      if (sizeof(Real) == 8) {
+        o[8] = (Real)kr; o[9] = (Real)ki; o[10] = (Real)qr; o[11] = (Real)qi;
+        o[12] = (Real)0; o[13] = (Real)0;
+      } else {
+        const double z[8][2] = {{kr, kr}, {-ki, ki}, {qr, qr}, {-qi, qi},
+                                {qr, qr}, {qi, -qi}, {kr, kr}, {ki, -ki}};
+        for (int i = 0; i < 8; ++i) {
+          o[32 + 2 * i] = (Real)z[i][0];
+          o[33 + 2 * i] = (Real)z[i][1];
+        }
+        o[48] = (Real)0; o[49] = (Real)0;
+      }
+    } else if (it.tan) {
       // deferred-factor rotation U = al (I + K): al = u00 = u11 (real for RX / RY runs),
       // K = off-diagonal / al.  XT (RX): K01 = K10 = i tau; RE (RY): K01 = rho, K10 = rho'.
       // The plain coefficients above stay for rows whose pass runs the plain variant.
@@ -189,6 +222,21 @@ __global__ void materialize_kernel(const MatArgs a) {
     }
   } else if (it.type == OP_U2F) {
     for (int k = 0; k < 32; ++k) out[it.mat_off + k] = (Real)a.fixed[2 * it.payload + k];
+  } else if (it.tan == 4) {
+    // derived phase of a kind-3 U1 op: Phi = diag(e^{i alpha}, e^{i beta}) = e^{i gamma} e^{i w Z},
+    // gamma = (alpha + beta) / 2 (term on mask 0), w = (alpha - beta) / 2 (Z term)
+    cdd M[4] = {{1, 0}, {0, 0}, {0, 0}, {1, 0}}, G[4];
+    for (int c = 0; c < it.cons_count; ++c) {
+      gate1(a.cons[it.cons_begin + c], th, a.fixed, G);
+      mat2mul(G, M, M);
+    }
+    const bool z0 = M[0].x == 0.0 && M[0].y == 0.0, z1 = M[3].x == 0.0 && M[3].y == 0.0;
+    const double al = z0 ? 0.0 : atan2(M[0].y, M[0].x), be = z1 ? 0.0 : atan2(M[3].y, M[3].x);
+    const double w = it.tan_idx ? 0.5 * (al - be) : 0.5 * (al + be);
+    double s, c;
+    sincos(w, &s, &c);
+    out[it.mat_off] = (Real)c;
+    out[it.mat_off + 1] = (Real)s;
   } else {
     const double w = it.param >= 0 ? it.w * th[it.param] : it.w;
     double s, c;
@@ -320,6 +368,20 @@ __global__ void finalize_kernel(const FinArgs a) {
     }
     // Pauli components of R' (device_common.cuh accum_c3): Im Tr(B R') = bx c0 + by c1 + bz c2
     const double c3[3] = {tot[g.acc + 0], tot[g.acc + 1], tot[g.acc + 2]};
+    // kind-3 ops (plan.cpp tan_kind_of): R' was accumulated before the diagonal phase Phi =
+    // diag(e^{i alpha}, e^{i beta}), so B' = Phi^dagger B Phi: B'01 = B01 e^{i (beta - alpha)}
+    cdd ph01 = {1, 0};
+    if (g.phase) {
+      cdd U[4] = {{1, 0}, {0, 0}, {0, 0}, {1, 0}}, G0[4];
+      for (int c = 0; c < g.cons_count; ++c) {
+        gate1(a.cons[g.cons_begin + c], th, a.fixed, G0);
+        mat2mul(G0, U, U);
+      }
+      const double r0 = sqrt(U[0].x * U[0].x + U[0].y * U[0].y), r1 = sqrt(U[3].x * U[3].x + U[3].y * U[3].y);
+      const cdd e0 = r0 > 0.0 ? cdd{U[0].x / r0, -U[0].y / r0} : cdd{1, 0};  // e^{-i alpha}
+      const cdd e1 = r1 > 0.0 ? cdd{U[3].x / r1, U[3].y / r1} : cdd{1, 0};   // e^{+i beta}
+      ph01 = cmul(e0, e1);
+    }
     cdd Sfx[4] = {{1, 0}, {0, 0}, {0, 0}, {1, 0}};
     for (int c = g.cons_count - 1; c >= 0; --c) {
       const DCons cn = a.cons[g.cons_begin + c];
@@ -333,7 +395,8 @@ __global__ void finalize_kernel(const FinArgs a) {
         mat2mul(Sfx, Pm, T1);
         mat2mul(T1, Sd, Bm);
         // B Hermitian traceless: B = bx X + by Y + bz Z, B01 = bx - i by, B00 = bz
-        const double bx = Bm[1].x, by = -Bm[1].y, bz = Bm[0].x;
+        const cdd b01 = cmul(Bm[1], ph01);
+        const double bx = b01.x, by = -b01.y, bz = Bm[0].x;
         ctb[cn.contrib] = cn.coeff * (bx * c3[0] + by * c3[1] + bz * c3[2]);
         if (a.qcontrib && g.re_acc >= 0)  // Im q = -coeff Re Tr(B R') / 2
           a.qcontrib[b * a.ncontrib + cn.contrib] =

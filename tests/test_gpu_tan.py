@@ -69,19 +69,27 @@ def extreme_thetas(B, P, seed):
     return th
 
 
-def with_tan(on, fn):
-    old = os.environ.get("TCX_NO_TAN")
-    if on:
-        os.environ.pop("TCX_NO_TAN", None)
-    else:
-        os.environ["TCX_NO_TAN"] = "1"
+def with_env(env, fn):
+    """Run fn with environment variables set (value None: unset); plan options are read when
+    a circuit is built."""
+    old = {k: os.environ.get(k) for k in env}
+    for k, v in env.items():
+        if v is None:
+            os.environ.pop(k, None)
+        else:
+            os.environ[k] = v
     try:
         return fn()
     finally:
-        if old is None:
-            os.environ.pop("TCX_NO_TAN", None)
-        else:
-            os.environ["TCX_NO_TAN"] = old
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def with_tan(on, fn, general=False):
+    return with_env({"TCX_NO_TAN": None if on else "1", "TCX_TAN_GENERAL": "1" if general else None}, fn)
 
 
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
@@ -151,3 +159,70 @@ def test_tan_matches_plain_qaoa(tc, dtype):
     for E, G in ((E1, G1), (E0, G0)):
         check_E(E, Er, H, dtype)
         check_grad(G, Gr, H, c, dtype)
+
+
+def general_circuit(n, layers, seed):
+    """General fused runs (kind 3: RX RY RZ / H S T mixes) between CNOT ladders in both
+    directions and CZ layers, so the derived diagonal phases sink through CNOT targets and
+    controls before they merge."""
+    rng = np.random.default_rng(seed)
+    c = W.Circuit(n, 0)
+    p = 0
+    for l in range(layers):
+        for q in range(n):
+            for g in rng.permutation(["rx", "ry", "rz", "h", "s", "t"])[:3]:
+                if g in ("rx", "ry", "rz"):
+                    c.add(str(g), q, param=p, coeff=1.0)
+                    p += 1
+                else:
+                    c.add(str(g), q)
+        if l % 3 == 0:
+            for q in range(n - 1):
+                c.add("cnot", q, q + 1)
+        elif l % 3 == 1:
+            for q in range(n - 1, 0, -1):
+                c.add("cnot", q, q - 1)
+        else:
+            for q in range(0, n - 1, 2):
+                c.add("cz", q, q + 1)
+    c.n_params = p
+    return c
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("n,t", [(6, None), (12, 8), (14, 9)])
+def test_general_runs_grad_vs_oracle(tc, dtype, n, t):
+    """Kind-3 factorisation (opt-in, TCX_TAN_GENERAL=1): (I + K) plus the derived diagonal phase."""
+    c = general_circuit(n, 5, 200 + n)
+    H = W.random_pauli_sum(n, 12, 3 * n)
+    th = extreme_thetas(4, c.n_params, 2 * n)
+    opts = {} if t is None else {"tile_bits": t, "coalesce_bits": 2}
+    C, P = with_tan(True, lambda: (tc.Circuit(c, dtype, **opts), tc.Pauli(H)), general=True)
+    E, G = tc.grad_batch(C, P, _th(th))
+    Er, Gr = orc.value_grad_batch(c, H, th, nthreads=os.cpu_count() or 1)
+    check_E(E.cpu().numpy(), Er, H, dtype, "general")
+    check_grad(G.cpu().numpy(), Gr, H, c, dtype, "general")
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_general_runs_state_and_hea(tc, dtype):
+    n = 13
+    c = general_circuit(n, 4, 9)
+    th = extreme_thetas(3, c.n_params, 10)
+    C = with_tan(True, lambda: tc.Circuit(c, dtype, tile_bits=8, coalesce_bits=2), general=True)
+    psi = tc.state_batch(C, _th(th)).cpu().numpy()
+    for b in range(th.shape[0]):
+        check_state(psi[b], orc.state(c, th[b]), dtype, len(c.gates), f"row {b}")
+    # HEA (cfg2 shape, smaller): deferred-factor plan == plain plan == oracle
+    c2, H2 = W.hea(14, 4), W.heisenberg(14)
+    th2 = W.thetas(4, c2.n_params, 11)
+
+    def run():
+        C2, P2 = tc.Circuit(c2, dtype, tile_bits=10), tc.Pauli(H2)
+        E, G = tc.grad_batch(C2, P2, _th(th2))
+        return E.cpu().numpy(), G.cpu().numpy()
+
+    Er, Gr = orc.value_grad_batch(c2, H2, th2, nthreads=os.cpu_count() or 1)
+    for E, G in (with_tan(True, run, general=True), with_tan(False, run)):
+        check_E(E, Er, H2, dtype)
+        check_grad(G, Gr, H2, c2, dtype)
