@@ -1079,7 +1079,7 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
   // kernels when tiles pair up and a sub-tile has whole warps
   // software-pipelined TMA tiles (prefetch of tile i+1 into its own buffer while tile i is
   // computed; the store of tile i drains while tile i+1 runs)
-  P.jit_pipe = getenv("TCX_JIT_PIPE") ? (atoi(getenv("TCX_JIT_PIPE")) != 0 ? 1 : 0) : -1;
+  P.jit_pipe = getenv("TCX_JIT_PIPE") ? std::min(2, std::max(0, atoi(getenv("TCX_JIT_PIPE")))) : -1;
   P.jit_nsub = 1;  // 2 = lock-stepped sub-tiles (measured slower with FFMA2 code; opt-in via TCX_JIT_NSUB)
   if (const char* e = getenv("TCX_JIT_NSUB"))
     if (atoi(e) == 2 && P.tpc % 2 == 0 && P.h >= 5) P.jit_nsub = 2;

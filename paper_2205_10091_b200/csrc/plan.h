@@ -221,7 +221,7 @@ struct Plan {
   int tpc = 1;                   // tiles per CTA (depends on the tile count only, never on B)
   int jit_nsub = 1;              // lock-stepped sub-tiles per CTA in JIT kernels
   std::vector<std::vector<std::pair<uint64_t, int>>> cut_sets;  // LUT cut tables (mask, sign)
-  int jit_pipe = -1;             // JIT TMA passes prefetch the next tile: 1 on, 0 off, -1 auto
+  int jit_pipe = -1;             // JIT TMA passes prefetch the next tile: 1 on, 0 off, 2 forward, -1 auto
   bool xchunk_forbid = false;     // sharded planning keeps the chunk bits out of post-exchange windows
   int xchunk_bits = 0;           // sharded: exchange column chunks = 2^xchunk_bits (overlap)
   bool cluster = false;          // cluster-resident: gbits = log2(CTAs per row), t = nloc
