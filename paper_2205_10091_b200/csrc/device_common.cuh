@@ -419,6 +419,12 @@ __device__ __forceinline__ void warp_sum3(Real (&r)[3], int lane, int width, Rea
   }
 }
 
+// One value: lane 0 writes its warp sum (structured U1 classes keep one slot, plan.cpp op_accs).
+template <typename Real>
+__device__ __forceinline__ void warp_sum1s(Real x, int lane, int width, Real* dst) {
+  x = warp_sum(x, width);
+  if (lane == 0) dst[0] = x;
+}
 // One component K of the three (structured classes): lane 0 writes it and zeroes the rest.
 template <int K, typename Real>
 __device__ __forceinline__ void warp_sum1(Real x, int lane, int width, Real* dst) {
@@ -544,7 +550,10 @@ __device__ __forceinline__ void op_bwd(const KOp& o, Cx<Real>* v, Cx<Real>* l,
       if (o.acc >= 0) {
         Real r[3] = {0, 0, 0};
         accum_c3<RB, k>(v, l, r);
-        warp_sum3(r, lane, width, wacc_w + o.acc);
+        if (o.nterm & 3)  // structured class: one slot, the component its generators read
+          warp_sum1s(r[(o.nterm & 3) - 1], lane, width, wacc_w + o.acc);
+        else
+          warp_sum3(r, lane, width, wacc_w + o.acc);
       }
       apply_u1_dag<RB, k>(v, m);
       apply_u1_dag<RB, k>(l, m);

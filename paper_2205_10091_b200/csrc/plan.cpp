@@ -381,8 +381,9 @@ thread_local bool g_q_grad = false;  // set per build_plan (this thread's plan)
 int op_accs(const Op& o) {
   if (!o.has_param) return 0;
   // U1: Pauli components (cX, cY, cZ) of R' (Im parts), + (rX, rY, rZ) real parts with
-  // q_grad; DIAG: one Im(lambda* psi) sum per slot, + one Re sum per slot
-  const int base = o.type == OP_U1 ? 3 : o.nslots;
+  // q_grad -- structured classes need one component (XT cX, RE cY, DG cZ); DIAG: one
+  // Im(lambda* psi) sum per slot, + one Re sum per slot
+  const int base = o.type == OP_U1 ? (u1_class_of(o.cons) ? 1 : 3) : o.nslots;
   return g_q_grad ? 2 * base : base;
 }
 
@@ -1611,7 +1612,8 @@ tcx_status build_plan(int n, int Pn, const tcx_gate* gates, int64_t G, const dou
         GItem gi{};
         gi.type = OP_U1;
         gi.acc = o.acc_off;
-        gi.re_acc = g_q_grad ? o.acc_off + 3 : -1;
+        gi.cls = u1_class_of(o.cons);
+        gi.re_acc = g_q_grad ? o.acc_off + (gi.cls ? 1 : 3) : -1;
         gi.cons_begin = mi.cons_begin;
         gi.cons_count = mi.cons_count;
         gi.contrib = -1;

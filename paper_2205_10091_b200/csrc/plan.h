@@ -106,9 +106,11 @@ struct GItem {       // finalize items
   int32_t cons_begin, cons_count;
   double factor;     // DIAG: -2 * w
   int32_t contrib;
-  int32_t re_acc;    // q_grad: slot of the real-part sums (U1: acc + 3), else -1
+  int32_t re_acc;    // q_grad: slot of the real-part sums (U1: acc + 3, structured acc + 1), else -1
   int32_t phase;     // U1 kind 3 (Op::tan): R' was taken before its diagonal phase, so the
-  int32_t pad;       //   generators are conjugated B' = Phi^dagger B Phi (finalize_kernel)
+                     //   generators are conjugated B' = Phi^dagger B Phi (finalize_kernel)
+  int32_t cls;       // U1 structured class (u1_class): 0 three slots (cX, cY, cZ), else the
+                     //   one component the class needs (1 cX, 2 cY, 3 cZ) in one slot
 };
 
 // Dense k-qubit block (north_star step 2): a run of gates fused into one

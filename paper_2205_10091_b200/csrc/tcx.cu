@@ -367,7 +367,13 @@ __global__ void finalize_kernel(const FinArgs a) {
       continue;
     }
     // Pauli components of R' (device_common.cuh accum_c3): Im Tr(B R') = bx c0 + by c1 + bz c2
-    const double c3[3] = {tot[g.acc + 0], tot[g.acc + 1], tot[g.acc + 2]};
+    // structured classes carry only the component their generators read (plan.cpp op_accs)
+    double c3[3] = {0.0, 0.0, 0.0}, r3[3] = {0.0, 0.0, 0.0};
+    for (int k = 0; k < 3; ++k) {
+      if (g.cls && k != g.cls - 1) continue;
+      c3[k] = tot[g.acc + (g.cls ? 0 : k)];
+      if (g.re_acc >= 0) r3[k] = tot[g.re_acc + (g.cls ? 0 : k)];
+    }
     // kind-3 ops (plan.cpp tan_kind_of): R' was accumulated before the diagonal phase Phi =
     // diag(e^{i alpha}, e^{i beta}), so B' = Phi^dagger B Phi: B'01 = B01 e^{i (beta - alpha)}
     cdd ph01 = {1, 0};
@@ -400,7 +406,7 @@ __global__ void finalize_kernel(const FinArgs a) {
         ctb[cn.contrib] = cn.coeff * (bx * c3[0] + by * c3[1] + bz * c3[2]);
         if (a.qcontrib && g.re_acc >= 0)  // Im q = -coeff Re Tr(B R') / 2
           a.qcontrib[b * a.ncontrib + cn.contrib] =
-              -0.5 * cn.coeff * (bx * tot[g.re_acc] + by * tot[g.re_acc + 1] + bz * tot[g.re_acc + 2]);
+              -0.5 * cn.coeff * (bx * r3[0] + by * r3[1] + bz * r3[2]);
       }
       cdd G[4];
       gate1(cn, th, a.fixed, G);
