@@ -600,12 +600,12 @@ void schedule_stages(Plan& P, const PassInfo& pass, std::vector<StageOut>& stage
   std::vector<char> done(pass.ops.size(), 0);
   size_t remaining = pass.ops.size();
   const int kStageAccMax = 256;
-  auto closure = [&](uint32_t R, std::vector<int>* out) {
+  auto closure_d = [&](const std::vector<char>& dn, uint32_t R, std::vector<int>* out) {
     uint64_t blocked = 0;
     double s = 0;
     int accs = 0;
     for (size_t i = 0; i < pass.ops.size(); ++i) {
-      if (done[i]) continue;
+      if (dn[i]) continue;
       const Op& o = P.ops[pass.ops[i]];
       bool ok = !(o.bits & blocked) && !(need[i] & ~R);
       if (ok && accs + op_accs(o) > kStageAccMax) ok = false;
@@ -625,21 +625,73 @@ void schedule_stages(Plan& P, const PassInfo& pass, std::vector<StageOut>& stage
   std::vector<uint32_t> cand;
   combos(t, r, cand);
   const uint32_t top = ((1u << t) - 1) & ~((1u << h) - 1);
+  auto greedy_pick = [&](const std::vector<char>& dn, double* score) {
+    double best = -1;
+    uint32_t R = top;
+    for (uint32_t m : cand) {
+      double sc = closure_d(dn, m, nullptr);
+      if (sc > best) {
+        best = sc;
+        R = m;
+      }
+    }
+    if (score) *score = best;
+    return R;
+  };
+  // Stage lookahead (round 2): each stage boundary costs a shared-memory exchange of the tile
+  // (plus two barriers), so among the best few greedy choices take the one whose greedy
+  // completion needs the fewest register-set changes, counting the return to the load/store
+  // set at the end.  TCX_STAGE_LOOKAHEAD=K candidates (0: plain greedy); big passes stay greedy.
+  static const int kLook = getenv("TCX_STAGE_LOOKAHEAD") ? atoi(getenv("TCX_STAGE_LOOKAHEAD")) : 4;
+  const bool look = kLook > 1 && pass.ops.size() <= 160;
+  auto finish_cost = [&](std::vector<char> dn, size_t rem, uint32_t R) {
+    int changes = 0;
+    uint32_t cur = R;
+    for (int guard = 0; rem > 0 && guard < 256; ++guard) {
+      const uint32_t nx = greedy_pick(dn, nullptr);
+      std::vector<int> idx;
+      closure_d(dn, nx, &idx);
+      if (idx.empty()) break;
+      for (int i : idx) dn[i] = 1;
+      rem -= idx.size();
+      if (nx != cur) ++changes;
+      cur = nx;
+    }
+    return changes + (cur != top ? 1 : 0);
+  };
   bool first = true;
+  uint32_t curR = top;
   while (remaining > 0 || first) {
     uint32_t R = top;
     if (!first) {
-      double best = -1;
-      for (uint32_t m : cand) {
-        double s = closure(m, nullptr);
-        if (s > best) {
-          best = s;
-          R = m;
+      if (!look) {
+        R = greedy_pick(done, nullptr);
+      } else {
+        std::vector<std::pair<double, uint32_t>> sc;
+        for (uint32_t m : cand) sc.push_back({closure_d(done, m, nullptr), m});
+        std::sort(sc.begin(), sc.end(), [](const std::pair<double, uint32_t>& a, const std::pair<double, uint32_t>& b) {
+          return a.first > b.first || (a.first == b.first && a.second < b.second);
+        });
+        int bestc = 1 << 30;
+        double bests = -1;
+        for (int k = 0; k < (int)sc.size() && k < kLook; ++k) {
+          if (sc[k].first <= 0) break;
+          std::vector<char> dn = done;
+          std::vector<int> idx;
+          closure_d(dn, sc[k].second, &idx);
+          for (int i : idx) dn[i] = 1;
+          const int c = (sc[k].second != curR ? 1 : 0) + finish_cost(dn, remaining - idx.size(), sc[k].second);
+          if (c < bestc || (c == bestc && sc[k].first > bests)) {
+            bestc = c;
+            bests = sc[k].first;
+            R = sc[k].second;
+          }
         }
+        if (bests < 0) R = sc.empty() ? top : sc[0].second;
       }
     }
     std::vector<int> idx;
-    closure(R, &idx);
+    closure_d(done, R, &idx);
     StageOut so;
     so.Rloc = R;
     for (int i : idx) {
@@ -649,6 +701,7 @@ void schedule_stages(Plan& P, const PassInfo& pass, std::vector<StageOut>& stage
     remaining -= idx.size();
     if (!first && idx.empty()) break;  // cannot happen (r >= arity); guard
     stages.push_back(std::move(so));
+    curR = R;
     first = false;
   }
 }
