@@ -154,6 +154,8 @@ typedef struct {
     int32_t cluster_bits;     /* cluster-resident plan: CTAs per theta row = 2^cluster_bits */
     int32_t exchange_overlaps; /* sharded: exchanges whose next pass (forward or backward) runs
                                   chunk by chunk as the exchange lands (overlap) */
+    int32_t tma_passes;       /* window passes whose tiles move by TMA (one box per tile) */
+    int32_t tma_multibox_passes; /* ... by TMA in 2^k boxes per tile (windows of > 5 runs) */
 } tcx_plan_info;
 
 typedef struct tcx_circuit tcx_circuit;

@@ -783,7 +783,26 @@ TmaDims tma_dims(int n, uint64_t wmask, bool c128) {
     runs.push_back({nbits, -1});
     in.push_back(0);
   }
-  if (runs.size() > 5) return d;  // rank 0: not expressible as one box
+  // multi-box windows (opt-in, TCX_TMA_MULTIBOX=1): measured slower on cfg3, whose scattered
+  // windows then move 8 boxes of 4 KB per tile (541 vs 584 circuits/s), so such windows keep
+  // plain coalesced loads by default
+  if (runs.size() > 5 && !getenv("TCX_TMA_MULTIBOX")) return d;  // rank 0: plain loads
+  if (runs.size() > 5) {
+    // multi-box: the first four runs form the box, dim 4 (box extent 1) is everything above;
+    // its window bits are iterated (at most 2^6 boxes per tile)
+    std::vector<int> sp;
+    for (size_t i = 4; i < runs.size(); ++i)
+      if (in[i])
+        for (int k = 0; k < runs[i].second; ++k) sp.push_back(runs[i].first + k);
+    if (sp.size() > 6) return d;  // rank 0: plain loads
+    const int s4 = runs[4].first;
+    runs.resize(4);
+    in.resize(4);
+    runs.push_back({s4, -1});
+    in.push_back(0);
+    d.sub = (int)sp.size();
+    for (int k = 0; k < d.sub; ++k) d.sub_pos[k] = sp[k];
+  }
   d.rank = (int)runs.size();
   for (int i = 0; i < d.rank; ++i) {
     d.start[i] = runs[i].first;
@@ -792,6 +811,10 @@ TmaDims tma_dims(int n, uint64_t wmask, bool c128) {
   }
   // innermost box >= 16 bytes
   if (!d.inwin[0] || (1 << d.bits[0]) * 8 < 16) d.rank = 0;
+  for (int i = 0; i < d.rank; ++i)
+    if (d.inwin[i]) d.kel += d.bits[i];
+  // multi-box: every box lands at a 128-byte aligned shared-memory address
+  if (d.sub && (8 << d.kel) < 128) d.rank = 0;
   return d;
 }
 

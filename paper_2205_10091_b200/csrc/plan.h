@@ -261,6 +261,12 @@ struct TmaDims {
   int bits[5];          // dim size 2^bits (the last dim also spans the batch: bits = -1)
   int inwin[5];         // 1: dim lies inside the window (box = full dim)
   int epa;              // 8-byte elements per amplitude
+  // multi-box windows (more runs than a rank-5 box holds): the box covers the first four runs,
+  // the window bits above them (inside dim 4) are iterated -- 2^sub boxes per tile, box j the
+  // contiguous chunk j << kel (elements) of the tile in shared memory
+  int sub = 0;          // iterated window bits
+  int kel = 0;          // element-index bits one box covers
+  int sub_pos[8];       // element-index positions of the iterated bits (increasing)
 };
 TmaDims tma_dims(int n, uint64_t wmask, bool c128);
 

@@ -2126,6 +2126,10 @@ tcx_status tcx_circuit_info(const tcx_circuit* circ, const tcx_pauli* pauli, tcx
   o->dense_blocks = (int)P.dblocks.size();
   o->init_h = __builtin_popcountll(P.init_hmask);
   o->cluster_bits = P.cluster ? P.gbits : 0;
+  for (const auto& ps : P.passes) {
+    const TmaDims td = tma_dims(P.nloc, ps.wmask, P.dtype == TCX_C128);
+    if (td.rank > 0 && !ps.ops.empty()) (td.sub ? o->tma_multibox_passes : o->tma_passes)++;
+  }
   for (size_t p = 1; p < P.passes.size(); ++p)
     if (P.passes[p].seg != P.passes[p - 1].seg)
       o->exchange_overlaps += pass_chunkable(P, P.passes[p]) + pass_chunkable(P, P.passes[p - 1]);

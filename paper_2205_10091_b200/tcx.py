@@ -55,7 +55,8 @@ class tcx_plan_info(ctypes.Structure):
         "threads_per_tile", "n_ops", "fwd_passes", "lambda_passes", "bwd_passes", "stages",
         "unitary", "relabeled", "jit", "global_bits", "segments")] + [(f, ctypes.c_int64) for f in (
             "tiles_per_state", "acc_slots", "mat_reals")] + [(f, ctypes.c_int32) for f in (
-            "dense_k", "dense_blocks", "init_h", "cluster_bits", "exchange_overlaps")]
+            "dense_k", "dense_blocks", "init_h", "cluster_bits", "exchange_overlaps",
+            "tma_passes", "tma_multibox_passes")]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

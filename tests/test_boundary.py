@@ -244,3 +244,23 @@ def test_cluster_plan_options():
         tcx.Circuit(W.hea(17, 1), "c64", cluster_bits=3)
     with pytest.raises(tcx.TcxError):  # complex128: at most 2^12 per CTA
         tcx.Circuit(W.hea(16, 1), "c128", cluster_bits=3)
+
+
+def test_tma_window_classes(tcx):
+    """cfg2's windows move their tiles by TMA boxes; cfg3's scattered windows need more index
+    runs than a rank-5 box holds, so they use plain coalesced loads unless multi-box tiles
+    (2^k boxes per tile, TCX_TMA_MULTIBOX=1) are enabled, which covers every pass."""
+    import os
+    name, c, H, th, dt = W.config(1, B=1)
+    i = tcx.Circuit(c, dt).info()
+    assert i["tma_passes"] == i["fwd_passes"] and i["tma_multibox_passes"] == 0, i
+    name, c, H, th, dt = W.config(2, B=1)
+    i0 = tcx.Circuit(c, dt).info()
+    assert i0["tma_multibox_passes"] == 0 and i0["tma_passes"] < i0["fwd_passes"], i0
+    os.environ["TCX_TMA_MULTIBOX"] = "1"
+    try:
+        i1 = tcx.Circuit(c, dt).info()
+    finally:
+        del os.environ["TCX_TMA_MULTIBOX"]
+    assert i1["tma_multibox_passes"] > 0, i1
+    assert i1["tma_passes"] + i1["tma_multibox_passes"] == i1["fwd_passes"], i1

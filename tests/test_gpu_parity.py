@@ -416,3 +416,47 @@ def test_l2_row_groups(tc, opts):
     Er, Gr = oracle_grad(c, H, th)
     check_E(E2, Er, H, "c64")
     check_grad(G2, Gr, H, c, "c64")
+
+
+def _scattered_circuit(n, layers, seed):
+    """Rotations and CNOTs on random qubit subsets: windows with many index runs (multi-box TMA
+    tiles, plan.cpp tma_dims)."""
+    rng = np.random.default_rng(seed)
+    c = W.Circuit(n, 0)
+    p = 0
+    for l in range(layers):
+        qs = rng.permutation(n)
+        for q in qs[: (2 * n) // 3]:
+            g = ("rx", "ry", "rz")[(l + int(q)) % 3]
+            c.add(g, int(q), param=p, coeff=1.0)
+            p += 1
+        for k in range(0, (2 * n) // 3 - 1, 2):
+            c.add("cnot", int(qs[k]), int(qs[k + 1]))
+        c.add("cz", int(qs[-1]), int(qs[-2]))
+    c.n_params = p
+    return c
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("t,cb", [(8, 1), (9, 1)])
+def test_multibox_tma_windows(tc, dtype, t, cb):
+    """Windows of more than five index runs move each tile as 2^k TMA boxes (state, E, grad
+    vs the oracle; the plan must really contain such passes)."""
+    n = 16
+    c = _scattered_circuit(n, 6, 40 + t)
+    H = W.random_pauli_sum(n, 10, 5)
+    th = W.thetas(3, c.n_params, 6)
+    # opt-in multi-box tiles: read when the plan is built, its kernels generated and launched
+    os.environ["TCX_TMA_MULTIBOX"] = "1"
+    try:
+        C, P = tc.Circuit(c, dtype, tile_bits=t, coalesce_bits=cb), tc.Pauli(H)
+        assert C.info()["tma_multibox_passes"] > 0, C.info()
+        E, G = tc.grad_batch(C, P, _th(th))
+        psi = tc.state_batch(C, _th(th)).cpu().numpy()
+    finally:
+        del os.environ["TCX_TMA_MULTIBOX"]
+    Er, Gr = oracle_grad(c, H, th)
+    check_E(E.cpu().numpy(), Er, H, dtype)
+    check_grad(G.cpu().numpy(), Gr, H, c, dtype)
+    for b in range(th.shape[0]):
+        check_state(psi[b], orc.state(c, th[b]), dtype, len(c.gates), f"row {b}")
