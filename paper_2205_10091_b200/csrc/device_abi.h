@@ -112,7 +112,7 @@ struct SmemLayout {
 TCX_HD inline int al16(int x) { return (x + 15) & ~15; }
 TCX_HD inline SmemLayout smem_layout(int t, int h, int realsz, int mat_count,
                                      int max_stage_acc, int acc_count, int nstages, bool two,
-                                     int nsub = 1, bool pipe = false) {
+                                     int nsub = 1, int pipe = 0) {
   // nsub lock-stepped sub-tiles per CTA (JIT kernels): one exchange buffer each
   SmemLayout L;
   int off = 0;
@@ -133,12 +133,13 @@ TCX_HD inline SmemLayout smem_layout(int t, int h, int realsz, int mat_count,
   L.red = off;
   off = al16(off + 8 * 32);
   // pipelined TMA passes: the next tile (psi, and lambda in two-state kernels) lands here
-  // while this one is computed (128-byte aligned TMA destination)
+  // while this one is computed (128-byte aligned TMA destination); pipe == 2 (two-state
+  // kernels, "half" pipeline) prefetches psi only, so two CTAs still fit one SM
   L.pb = 0;
   if (pipe) {
     off = (off + 127) & ~127;
     L.pb = off;
-    off += (two ? 2 : 1) * (csz << t);
+    off += ((two && pipe == 1) ? 2 : 1) * (csz << t);
   }
   L.total = off;
   return L;

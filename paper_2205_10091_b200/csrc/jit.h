@@ -27,5 +27,5 @@ std::string jit_kernel_name(const std::string& key);
 // or without the backward: on when the plan asks for it, the window is a TMA box and the
 // prefetch buffer still fits the 227 KB of shared memory
 struct PassInfo;
-bool jit_pipe_on(const Plan& P, const PassInfo& p, bool bwd);
+int jit_pipe_on(const Plan& P, const PassInfo& p, bool bwd);
 }  // namespace tcx

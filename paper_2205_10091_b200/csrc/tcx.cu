@@ -870,6 +870,14 @@ WsLayout ws_layout(const Plan& P, const Binding* Bd, int64_t B, int kind, bool h
   const bool need_psi = !w.mega;
   const bool need_lam = kind == K_GRAD && !w.mega;
   w.psi = need_psi ? take(B * N * 2 * rs) : 0;
+  // psi and lambda tiles are read and written together at the same relative offset; with a
+  // power-of-two state array they would sit exactly 2^k bytes apart (same DRAM channel / L2
+  // set hash for every pair), so lambda starts a small odd number of 256-byte units later
+  static const size_t lam_pad = [] {
+    const char* e = getenv("TCX_LAM_PAD");
+    return e ? (size_t)atoll(e) : (size_t)0;
+  }();
+  if (need_lam && lam_pad) off = align256(off + lam_pad);
   w.lam = need_lam ? take(B * N * 2 * rs) : 0;
   w.mats = take(B * std::max(P.mat_total, 1) * rs);
   w.part = kind == K_GRAD ? take(B * S * std::max(P.acc_total, 1) * 8) : 0;
@@ -1458,7 +1466,7 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
             a.use_tma = (wl.lam == 0 || encode_tmap(a.tmap[1], a.lam, td, P.nloc, B)) ? 1 : 0;
           if (!(a.mode & (M_LOAD_PSI | M_LOAD_LAM | M_STORE_PSI | M_STORE_LAM))) a.use_tma = 0;
         }
-        const bool pipe = jkey[0] == 'p' && jit_pipe_on(P, P.passes[jit_key_pass_index(jkey)], two);
+        const int pipe = jkey[0] != 'p' ? 0 : jit_pipe_on(P, P.passes[jit_key_pass_index(jkey)], two);
         const SmemLayout LJ = smem_layout(a.t, a.h, rs, a.mat_count, a.max_stage_acc,
                                           (a.mode & M_BWD) ? a.acc_count : 0, a.nstages, two, ns, pipe);
         if (LJ.total > 227 * 1024 - 1280)
