@@ -18,7 +18,9 @@ def load(path):
         v = float(r["Metric Value"].replace(",", ""))
         unit = r.get("Metric Unit", "")
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
-                 "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}.get(unit, 1.0)
+                 "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9, "TB": 1e12,
+                 "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0,
+                 "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0}.get(unit, 1.0)
         d[r["Metric Name"]] = v * scale
     return rows
 
