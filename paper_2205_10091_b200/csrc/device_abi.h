@@ -98,6 +98,10 @@ struct PassArgs {
   // partial slot is b * cta_stride + cta_base + blockIdx.x (cta_stride = CTAs per full launch)
   int chunk_pos, chunk_bits, chunk_val, cta_base;
   int64_t cta_stride;
+  // tile order of the JIT pass kernels: 0 blocked (CTA x takes tiles [x*tpc, (x+1)*tpc)),
+  // 1 interleaved (CTA x takes tiles it*gridDim.x + x; tcx.cu picks it when a row's CTAs are
+  // co-resident, so the two halves of a line shared by neighbouring tiles are read together)
+  int tile_ilv, pad_ilv;
 };
 // tile index of a (possibly chunked) launch: the chunk value inserted at chunk_pos
 TCX_HD inline int64_t chunk_tile(int64_t t, int pos, int bits, int val) {

@@ -851,6 +851,22 @@ int dense_max_k(const Plan& P) {
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// JIT pass kernels: interleaved tile order (PassArgs.tile_ilv) when a launch has at most two
+// CTAs per SM per row; TCX_TILE_ORDER=0/1 forces blocked / interleaved for A/B runs
+int tile_order_ilv(int64_t ctas_per_row) {
+  static const int forced = [] {
+    const char* e = getenv("TCX_TILE_ORDER");
+    return e ? atoi(e) : -1;
+  }();
+  if (forced >= 0) return forced ? 1 : 0;
+  static int nsm[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 0;
+  if (!nsm[dev] && cudaDeviceGetAttribute(&nsm[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return 0;
+  return ctas_per_row <= 2 * (int64_t)nsm[dev] ? 1 : 0;
+}
+
 WsLayout ws_layout(const Plan& P, const Binding* Bd, int64_t B, int kind, bool host_io,
                    bool inputs = false) {
   WsLayout w{};
@@ -1412,6 +1428,7 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
     a.cta_stride = S;
     a.cta_base = 0;
     a.chunk_bits = 0;
+    a.tile_ilv = 0;
   };
   auto set_pass = [&](PassArgs& a, const PassInfo& p, bool with_ops) {
     a.stages = (const KStage*)DT->kstages.p + p.stage_begin;
@@ -1453,6 +1470,9 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
       a.chunk_val = one->chunk;
       a.cta_base = (int)(one->chunk * Sg);
     }
+    // interleaved tile order when the CTAs of a row are co-resident (a few rows' worth fit the
+    // GPU at once: cfg2 / cfg3), blocked otherwise (one huge row: cfg5 measured slower with it)
+    a.tile_ilv = tile_order_ilv(Sg);
     for (int64_t b0 = rlo; b0 < rhi; b0 += kMaxRows) {
       const int64_t rows = std::min(kMaxRows, rhi - b0);
       a.b0 = b0;
