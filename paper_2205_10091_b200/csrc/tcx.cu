@@ -860,11 +860,15 @@ int tile_order_ilv(int64_t ctas_per_row) {
   }();
   if (forced >= 0) return forced ? 1 : 0;
   static int nsm[64] = {0};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 0;
-  if (!nsm[dev] && cudaDeviceGetAttribute(&nsm[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-    return 0;
-  return ctas_per_row <= 2 * (int64_t)nsm[dev] ? 1 : 0;
+  int dev = 0, sms = 148;  // B200; used when no device is visible (plan-time on a CPU host)
+  if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64) {
+    if (!nsm[dev] && cudaDeviceGetAttribute(&nsm[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      nsm[dev] = 148;
+    sms = nsm[dev];
+  } else {
+    cudaGetLastError();
+  }
+  return ctas_per_row <= 2 * (int64_t)sms ? 1 : 0;
 }
 
 WsLayout ws_layout(const Plan& P, const Binding* Bd, int64_t B, int kind, bool host_io,
@@ -1812,6 +1816,50 @@ tcx_status tcx_circuit_build(int32_t n_qubits, int32_t n_params, const tcx_gate*
   if (s) {
     delete c;
     return fail(s, err);
+  }
+  // Contiguous-run width (coalesce_bits) when the caller leaves it to the library: every
+  // window holds the lowest c index bits, so c trades the length of the contiguous runs a tile
+  // is made of against the freedom of the light-cone windows (fewer passes).  The neighbours
+  // c - 1 and c + 1 of the default are planned too and the plan with the lowest
+  // passes x w(run bytes) wins, w = 1.0 (128-byte runs), 1.1 (64), 1.25 (32, interleaved tile
+  // order: the rest of each line is read by concurrent CTAs) or 1.5 (32, blocked order); runs
+  // under 32 bytes (a partial sector) are not considered.  The weights are the session-3
+  // measurements (profiles/bench_r2_s3_*.jsonl): cfg3 8 passes of 128-byte runs beat 7 of
+  // 32-byte runs (623 vs 598 circuits/s), cfg5 4 passes of 32-byte runs beat 7 of 64 (0.638 vs
+  // 0.618), cfg4 86 passes of 64-byte runs beat 74 of 32 (0.404 vs 0.355), cfg2 6 of 128
+  // beat 7 of 64 (3671 vs 3635).  TCX_AUTO_COALESCE=0 keeps the default width.
+  {
+    static const bool auto_c = !(getenv("TCX_AUTO_COALESCE") && atoi(getenv("TCX_AUTO_COALESCE")) == 0);
+    const Plan& P0 = c->plan;
+    const int c0 = P0.c, t0 = P0.t;  // P0 goes away if a neighbour wins
+    const int asz = dtype == TCX_C128 ? 16 : 8;
+    auto cost = [&](const Plan& A) {
+      const int run = asz << A.c;
+      const int64_t ctas_per_row = A.tiles / std::max(A.tpc, 1);
+      double w = run >= 128 ? 1.0 : (run >= 64 ? 1.1 : (tile_order_ilv(ctas_per_row) ? 1.25 : 1.5));
+      return (double)A.passes.size() * w;
+    };
+    if (auto_c && (!opts || opts->coalesce_bits <= 0) && P0.gbits == 0 && !P0.cluster &&
+        P0.dblocks.empty() && (int64_t)P0.tiles > 1 && (!opts || opts->dense_k <= 0)) {
+      tcx_build_opts o2{};
+      if (opts) o2 = *opts;
+      for (int dc : {-1, 1}) {
+        o2.coalesce_bits = c0 + dc;
+        if (o2.coalesce_bits < 1 || t0 - o2.coalesce_bits < 2 || (asz << o2.coalesce_bits) < 32) continue;
+        tcx_circuit* alt = new (std::nothrow) tcx_circuit();
+        if (!alt) break;
+        std::string e2;
+        tcx_status s2;
+        try {
+          s2 = build_plan(n_qubits, n_params, gates, n_gates, matrices, n_matrix_elems, dtype, &o2,
+                          alt->plan, e2);
+        } catch (const std::bad_alloc&) {
+          s2 = TCX_E_OOM;
+        }
+        if (s2 == TCX_OK && cost(alt->plan) < cost(c->plan)) std::swap(c, alt);
+        delete alt;
+      }
+    }
   }
   if (c->plan.gbits > 0 && !getenv("TCX_SHARD_NO_LAYOUT_SEARCH")) {
     // Sharded layout search.  The exchange always swaps the g global bits (qubits 0..g-1,

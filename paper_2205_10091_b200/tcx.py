@@ -8,6 +8,7 @@ infrastructure and is never imported here).
 from __future__ import annotations
 
 import ctypes
+import weakref
 import os
 from typing import Optional
 
@@ -262,18 +263,24 @@ class Workspace:
     queued there may still touch it."""
 
     def __init__(self):
-        self._buf = {}
+        # circuit -> {(pauli, B, mode, device, stream): buffer}; weak on the circuit, so a
+        # circuit's scratch memory is released with it (a plain dict keyed by id(circ) kept
+        # every workspace alive for the life of the process)
+        self._buf = weakref.WeakKeyDictionary()
 
     def get(self, circ, pauli, B, mode, device, stream=None):
         torch = _torch()
         s = stream if stream is not None else torch.cuda.current_stream(device)
-        key = (id(circ), id(pauli) if pauli else 0, B, mode, str(device), s.cuda_stream)
+        key = (id(pauli) if pauli else 0, B, mode, str(device), s.cuda_stream)
         need = circ.workspace_bytes(pauli, B, mode)
-        buf = self._buf.get(key)
+        per = self._buf.setdefault(circ, {})
+        buf = per.get(key)
         if buf is None or buf.numel() < need:
+            per.pop(key, None)  # release the smaller buffer before allocating the larger one
+            buf = None
             with torch.cuda.stream(s):  # allocated on the stream that uses it
                 buf = torch.empty(max(need, 16), dtype=torch.uint8, device=device)
-            self._buf[key] = buf
+            per[key] = buf
         return buf, need
 
     def clear(self):

@@ -255,11 +255,11 @@ def test_tma_window_classes(tcx):
     i = tcx.Circuit(c, dt).info()
     assert i["tma_passes"] == i["fwd_passes"] and i["tma_multibox_passes"] == 0, i
     name, c, H, th, dt = W.config(2, B=1)
-    i0 = tcx.Circuit(c, dt).info()
+    i0 = tcx.Circuit(c, dt, coalesce_bits=3).info()  # 64-byte runs (the width is otherwise auto)
     assert i0["tma_multibox_passes"] == 0 and i0["tma_passes"] < i0["fwd_passes"], i0
     os.environ["TCX_TMA_MULTIBOX"] = "1"
     try:
-        i1 = tcx.Circuit(c, dt).info()
+        i1 = tcx.Circuit(c, dt, coalesce_bits=3).info()
     finally:
         del os.environ["TCX_TMA_MULTIBOX"]
     assert i1["tma_multibox_passes"] > 0, i1

@@ -75,6 +75,7 @@ def _run(c, H, th, shard_g=0, expect_only=False):
     import torch
     from paper_2205_10091_b200 import tcx
     from paper_2205_10091_b200.shard import ShardedState
+    _free()  # earlier modules' circuits (and their cached workspaces) must be gone first
     if shard_g:
         S = ShardedState(c, H, "c64", shard_g)
         E, G = S.run(_th(th), want_grad=not expect_only)
