@@ -264,3 +264,22 @@ def test_tma_window_classes(tcx):
         del os.environ["TCX_TMA_MULTIBOX"]
     assert i1["tma_multibox_passes"] > 0, i1
     assert i1["tma_passes"] + i1["tma_multibox_passes"] == i1["fwd_passes"], i1
+
+
+def test_auto_run_width(tcx):
+    """coalesce_bits = 0 lets the library plan c - 1, c, c + 1 and keep the lowest
+    passes x run-length weight (DESIGN §6 "Run width per plan"): 128-byte runs for cfg2 / cfg3,
+    32-byte runs for cfg5 (7 -> 4 passes), the 64-byte default for complex128 cfg4; an explicit
+    width is kept as given, and the auto choice never plans more passes x weight than it."""
+    want = {1: 4, 2: 4, 3: 2, 4: 2}
+    for idx, cw in want.items():
+        name, c, H, th, dt = W.config(idx, B=1)
+        auto = tcx.Circuit(c, dt).info()
+        assert auto["coalesce_bits"] == cw, (name, auto)
+        asz = 16 if dt == "c128" else 8
+        assert (asz << auto["coalesce_bits"]) >= 32, (name, auto)
+        for cb in (cw - 1, cw, cw + 1):
+            i = tcx.Circuit(c, dt, coalesce_bits=cb).info()
+            assert i["coalesce_bits"] == cb, (name, cb, i)
+            if cb == cw:
+                assert i["fwd_passes"] == auto["fwd_passes"], (name, i, auto)

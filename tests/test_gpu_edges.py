@@ -79,3 +79,22 @@ def test_identity_and_empty_pauli_sums(tc):
     empty = W.PauliSum(7, np.zeros((0, 7), np.uint8), np.zeros(0))
     E0 = tc.expect_batch(C, tc.Pauli(empty), _th(th)).cpu().numpy()
     assert np.all(E0 == 0.0)
+
+
+def test_default_workspace_released_with_circuit(tc):
+    """The binding's default workspace cache is weak on the circuit: a circuit's scratch
+    memory goes away with it (an id-keyed cache kept every workspace of the process alive)."""
+    import gc
+    import torch
+    name, c, H, th, dt = W.config(1, B=4, n=14)
+    C, P = tc.Circuit(c, dt), tc.Pauli(H)
+    E, G = tc.grad_batch(C, P, _th(th))
+    torch.cuda.synchronize()
+    assert C in tc._default_ws._buf
+    buf = next(iter(tc._default_ws._buf[C].values()))
+    assert buf.numel() >= C.workspace_bytes(P, 4, 1)
+    before = torch.cuda.memory_allocated()
+    del C, buf
+    gc.collect()
+    assert torch.cuda.memory_allocated() < before
+    assert np.isfinite(G.cpu().numpy()).all()
