@@ -1862,9 +1862,13 @@ std::shared_ptr<Binding> bind(Plan& P, const Pauli& H) {
     left.swap(rest);
     B->units.push_back(u);
   };
+  // lambda-unit windows keep at least the default run width (64-byte runs) even when the
+  // passes use shorter ones: the units read psi and read-modify-write lambda in blocked tile
+  // order, where 32-byte runs waste DRAM bursts (cfg5: 137 -> 251 ms of lambda units)
+  const int cl = (P.gbits == 0 && !getenv("TCX_LAM_SAME_C")) ? std::max(c, P.dtype == TCX_C128 ? 2 : 3) : c;
   auto greedy_units = [&]() {
     while (!left.empty()) {
-      uint64_t W = (1ull << c) - 1;
+      uint64_t W = (1ull << std::min(cl, t)) - 1;
       bool grew = true;  // admit groups in order of fewest extra bits
       while (grew) {
         grew = false;
