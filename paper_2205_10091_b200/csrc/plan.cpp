@@ -1862,10 +1862,11 @@ std::shared_ptr<Binding> bind(Plan& P, const Pauli& H) {
     left.swap(rest);
     B->units.push_back(u);
   };
-  // lambda-unit windows keep at least the default run width (64-byte runs) even when the
-  // passes use shorter ones: the units read psi and read-modify-write lambda in blocked tile
-  // order, where 32-byte runs waste DRAM bursts (cfg5: 137 -> 251 ms of lambda units)
-  const int cl = (P.gbits == 0 && !getenv("TCX_LAM_SAME_C")) ? std::max(c, P.dtype == TCX_C128 ? 2 : 3) : c;
+  // lambda-unit windows use the default run width (64-byte runs) whatever the passes use: the
+  // units read psi and read-modify-write lambda in blocked tile order, where 32-byte runs waste
+  // DRAM bursts (cfg5: 238 -> 139 ms of lambda units), and 128-byte runs leave fewer free
+  // window bits (cfg2: two units instead of one)
+  const int cl = (P.gbits == 0 && !getenv("TCX_LAM_SAME_C")) ? (P.dtype == TCX_C128 ? 2 : 3) : c;
   auto greedy_units = [&]() {
     while (!left.empty()) {
       uint64_t W = (1ull << std::min(cl, t)) - 1;
