@@ -143,7 +143,7 @@ TCX_HD inline SmemLayout smem_layout(int t, int h, int realsz, int mat_count,
   if (pipe) {
     off = (off + 127) & ~127;
     L.pb = off;
-    off += ((two && pipe == 1) ? 2 : 1) * (csz << t);
+    off += (((two && pipe == 1) || pipe == 3) ? 2 : 1) * (csz << t);  // 3: two one-state buffers
   }
   L.total = off;
   return L;
