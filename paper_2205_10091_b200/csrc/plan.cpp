@@ -503,19 +503,12 @@ struct Scheduler {
     const uint64_t base = (1ull << c) - 1;
     uint64_t bestW = 0;
     double best = -1;
-    // TCX_PLAN_TMA_ONLY: a window whose tile is a TMA box beats any that is not (the
-    // scattered windows fall back to per-thread loads); non-box windows only when no
-    // candidate is a box
-    static const bool tma_only = getenv("TCX_PLAN_TMA_ONLY") != nullptr;
-    bool bestT = false;
     auto consider = [&](uint64_t W) {
       double s = closure(W, nullptr);
-      const bool T = tma_only && tma_ok(W);
       if (all) all->push_back({s, W});
-      if ((T && !bestT) || (T == bestT && s > best)) {
+      if (s > best) {
         best = s;
         bestW = W;
-        bestT = T;
       }
     };
     auto fill = [&](uint64_t W) {  // pad with lowest unused bits
@@ -573,10 +566,6 @@ struct Scheduler {
       for (int b = s; b < s + (t - c); ++b) W |= 1ull << b;
       if (!(W & forbid)) consider(W);
     }
-    if (all && bestT)
-      all->erase(std::remove_if(all->begin(), all->end(),
-                                [&](const std::pair<double, uint64_t>& x) { return !tma_ok(x.second); }),
-                 all->end());
     return bestW;
   }
 };
