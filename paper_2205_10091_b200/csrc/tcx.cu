@@ -858,7 +858,7 @@ int tile_order_ilv(int64_t ctas_per_row) {
     const char* e = getenv("TCX_TILE_ORDER");
     return e ? atoi(e) : -1;
   }();
-  if (forced >= 0) return forced ? 1 : 0;
+  if (forced >= 0) return forced;  // 0 blocked, 1 interleaved, g >= 2 groups of g CTAs
   static int nsm[64] = {0};
   int dev = 0, sms = 148;  // B200; used when no device is visible (plan-time on a CPU host)
   if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64) {
@@ -1477,6 +1477,7 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
     // interleaved tile order when the CTAs of a row are co-resident (a few rows' worth fit the
     // GPU at once: cfg2 / cfg3), blocked otherwise (one huge row: cfg5 measured slower with it)
     a.tile_ilv = tile_order_ilv(Sg);
+    if (a.tile_ilv >= 2 && (Sg % a.tile_ilv)) a.tile_ilv = 0;  // groups must tile the grid
     for (int64_t b0 = rlo; b0 < rhi; b0 += kMaxRows) {
       const int64_t rows = std::min(kMaxRows, rhi - b0);
       a.b0 = b0;
