@@ -851,9 +851,9 @@ int dense_max_k(const Plan& P) {
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-// JIT pass kernels: interleaved tile order (PassArgs.tile_ilv) when a launch has at most two
-// CTAs per SM per row; TCX_TILE_ORDER=0/1 forces blocked / interleaved for A/B runs
-int tile_order_ilv(int64_t ctas_per_row) {
+// JIT pass kernels: interleaved tile order (PassArgs.tile_ilv = 1) when a launch has at most two
+// CTAs per SM per row, else blocked (0) or grouped (g); TCX_TILE_ORDER=0/1/g forces one for A/B
+int tile_order_ilv(int64_t ctas_per_row, int run_bytes) {
   static const int forced = [] {
     const char* e = getenv("TCX_TILE_ORDER");
     return e ? atoi(e) : -1;
@@ -868,7 +868,11 @@ int tile_order_ilv(int64_t ctas_per_row) {
   } else {
     cudaGetLastError();
   }
-  return ctas_per_row <= 2 * (int64_t)sms ? 1 : 0;
+  if (ctas_per_row <= 2 * (int64_t)sms) return 1;
+  // one huge row: blocked order, but 32-byte runs go in groups of 4 neighbouring CTAs so the
+  // four sectors of a line are read together (cfg5 backward: 367 -> 142 GB of DRAM reads per
+  // pass for 137 GB of psi and lambda, 0.685 -> 0.692 circuits/s; session 3, t16)
+  return run_bytes <= 32 ? 4 : 0;
 }
 
 WsLayout ws_layout(const Plan& P, const Binding* Bd, int64_t B, int kind, bool host_io,
@@ -1476,7 +1480,7 @@ tcx_status run(Plan& P, const tcx_pauli* H, const double* theta, int64_t B, doub
     }
     // interleaved tile order when the CTAs of a row are co-resident (a few rows' worth fit the
     // GPU at once: cfg2 / cfg3), blocked otherwise (one huge row: cfg5 measured slower with it)
-    a.tile_ilv = tile_order_ilv(Sg);
+    a.tile_ilv = tile_order_ilv(Sg, (rs * 2) << P.c);
     if (a.tile_ilv >= 2 && (Sg % a.tile_ilv)) a.tile_ilv = 0;  // groups must tile the grid
     for (int64_t b0 = rlo; b0 < rhi; b0 += kMaxRows) {
       const int64_t rows = std::min(kMaxRows, rhi - b0);
@@ -1837,7 +1841,7 @@ tcx_status tcx_circuit_build(int32_t n_qubits, int32_t n_params, const tcx_gate*
     auto cost = [&](const Plan& A) {
       const int run = asz << A.c;
       const int64_t ctas_per_row = A.tiles / std::max(A.tpc, 1);
-      double w = run >= 128 ? 1.0 : (run >= 64 ? 1.1 : (tile_order_ilv(ctas_per_row) ? 1.25 : 1.5));
+      double w = run >= 128 ? 1.0 : (run >= 64 ? 1.1 : (tile_order_ilv(ctas_per_row, run) == 1 ? 1.25 : 1.5));
       return (double)A.passes.size() * w;
     };
     if (auto_c && (!opts || opts->coalesce_bits <= 0) && P0.gbits == 0 && !P0.cluster &&
